@@ -1,0 +1,61 @@
+// device.cuh -- layouts and descriptors shared by the host orchestrator and
+// the sm_100a kernels of the Jacobi3D hot path.
+//
+// HBM layout of one block buffer:
+//   a ghosted 3D array of (nz+2) planes x (ny+2) rows x pitch doubles.  Owned
+//   cell (x,y,z), x in [0,nx), lives at
+//       base[(z+1)*zs + (y+1)*pitch + XOFF + x],   zs = pitch*(ny+2)
+//   with the -x ghost at column XOFF-1 and the +x ghost at XOFF+nx.  XOFF = 16
+//   doubles puts every owned row on a 128-byte boundary (pitch is a multiple
+//   of 16 doubles and buffers are 256-byte aligned), so warps read and write
+//   whole 128-byte lines and 16-byte vector accesses are aligned.
+#pragma once
+#include <cstdint>
+
+namespace j3d {
+
+constexpr int XOFF = 16;
+constexpr int PITCH_ALIGN = 16;  // doubles
+
+struct FaceRef {  // element (a,b) of a 2D face lives at p[a*sa + b*sb]
+    double* p;
+    int64_t sa, sb;
+};
+
+// One (block, buffer parity) as seen by the stencil kernel.
+struct StencilDesc {
+    const double* in;   // ghosted input buffer  (u^n)
+    double* out;        // ghosted output buffer (u^{n+1})
+    int32_t nx, ny, nz;
+    uint32_t epi_mask;  // faces whose new boundary layer the epilogue stores to epi[f]
+    int64_t pitch, zs;
+    uint32_t pro_mask;  // faces whose ghost values the prologue reads from pro[f]
+    uint32_t pad;
+    FaceRef epi[6];
+    FaceRef pro[6];
+};
+
+// A unit of stencil work: one (TX x TY) tile of one block over planes [z0,z1).
+struct WorkItem {
+    int32_t blk;    // local block index (descriptor = 2*blk + parity)
+    int16_t tx, ty; // tile coordinates
+    int32_t z0, z1;
+};
+
+// A strided 2D face copy (pack: owned layer -> send buffer / peer receive
+// buffer; unpack: receive buffer -> ghost layer).  na == 0 marks an unused slot.
+struct CopyDesc {
+    FaceRef src;
+    FaceRef dst;
+    int32_t na, nb;
+};
+
+// Per-block geometry for init / checksum / residual.
+struct BlockGeom {
+    double* buf[2];
+    int64_t ox, oy, oz;  // global origin of owned cell (0,0,0)
+    int32_t nx, ny, nz, pad;
+    int64_t pitch, zs;
+};
+
+}  // namespace j3d

@@ -1,0 +1,40 @@
+// kernels.h -- host-side launch interface of the sm_100a kernels (kernels.cu).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device.cuh"
+
+namespace j3d {
+
+struct TileShape {
+    int tx, ty;
+};
+
+struct StencilLaunch {
+    const StencilDesc* descs;  // device, [2*n_local_blocks]
+    const CUtensorMap* tmaps;  // device, [2*n_local_blocks], 64-B aligned
+    const WorkItem* items;     // device
+    int n_items;
+    int parity;  // input buffer parity
+    int grid;    // persistent CTAs
+    int kind;    // tile kind (0: 128x16, 1: 64x16)
+    bool faces;  // any prologue/epilogue faces in this launch
+};
+
+TileShape tile_shape(int kind);
+int stencil_box_w(int kind);
+int stencil_box_h(int kind);
+cudaError_t launch_stencil(const StencilLaunch& L, cudaStream_t st);
+cudaError_t stencil_occupancy(int kind, bool faces, int* blocks_per_sm);
+cudaError_t launch_copy_faces(const CopyDesc* d, int per_group, int groups, int64_t max_cells, cudaStream_t st);
+cudaError_t launch_init(const BlockGeom* g, int nblocks, int max_nx, int64_t max_rows, int kind, const double* p,
+                        uint64_t seed, double boundary, int64_t gx, int64_t gy, int64_t gz, cudaStream_t st);
+cudaError_t launch_checksum(const BlockGeom* g, int nblocks, int which, int64_t gx, int64_t gy,
+                            unsigned long long* acc, int sms, cudaStream_t st);
+cudaError_t launch_residual(const BlockGeom* g, int nblocks, int which, unsigned long long* acc, int sms,
+                            cudaStream_t st);
+
+}  // namespace j3d

@@ -1,0 +1,71 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times, on sampled outputs the oracle computes one by one from their
+dependency cones (tests/helpers.cone_value), plus properties that hold at
+any size.  Needs ~60 GB of HBM."""
+import numpy as np
+import pytest
+
+from tests.helpers import cone_value
+
+pytestmark = pytest.mark.gpu
+
+j3d = pytest.importorskip("paper_2202_11819_b200")
+
+SEED = 20220223
+
+
+def _samples(grid, ext, rng, n_random=24):
+    gx, gy, gz = grid
+    cells = set()
+    for i in (0, gx - 1):
+        for j in (0, gy - 1):
+            for k in (0, gz - 1):
+                cells.add((i, j, k))
+    # cells on both sides of every internal block face (where the exchange matters)
+    for a, (g, e) in enumerate(zip(grid, ext)):
+        for b in range(e, g, e):
+            for side in (b - 1, b):
+                c = [int(rng.integers(0, grid[0])), int(rng.integers(0, grid[1])), int(rng.integers(0, grid[2]))]
+                c[a] = side
+                cells.add(tuple(c))
+    for _ in range(n_random):
+        cells.add(tuple(int(rng.integers(0, g)) for g in grid))
+    return sorted(cells)
+
+
+def _check(ctx, grid, n, rng):
+    ext = ctx.extent
+    for (i, j, k) in _samples(grid, ext, rng):
+        bid = (i // ext[0]) + (grid[0] // ext[0]) * ((j // ext[1]) + (grid[1] // ext[1]) * (k // ext[2]))
+        (ox, oy, oz), _, owner = ctx.block_info(bid)
+        got = ctx.get_region(bid, (i - ox, j - oy, k - oz), (1, 1, 1))[0, 0, 0]
+        want = cone_value(grid, SEED, n, (i, j, k))
+        assert np.float64(got).tobytes() == np.float64(want).tobytes(), ((i, j, k), got, want)
+
+
+@pytest.mark.parametrize("odf,variant", [(1, "direct"), (8, "direct"), (8, "unfused"), (8, "C")])
+def test_weak_1536_sampled(odf, variant):
+    """configs[1]/[2]: 1536^3 per GPU, ODF 1 and 8, hash-random interior (seed
+    20220223), 3 iterations, batched launch (bench.py's configuration)."""
+    grid = (1536, 1536, 1536)
+    rng = np.random.default_rng(odf)
+    with j3d.Jacobi3D(grid, odf=odf, variant=variant, launch="batched") as ctx:
+        ctx.init("hash", seed=SEED)
+        ctx.iterate(3)
+        ctx.synchronize()
+        _check(ctx, grid, 3, rng)
+        r = ctx.residual()
+        assert 0.0 < r <= 1.0
+
+
+def test_weak_1536_fixed_point_at_scale():
+    """Property at full size: a linear field is a bitwise fixed point, so the
+    GPU checksum after 10 iterations equals the checksum of the initial
+    state (the oracle's checksum definition on the GPU's own init)."""
+    grid = (1536, 1536, 1536)
+    with j3d.Jacobi3D(grid, odf=1, variant="direct") as ctx:
+        ctx.init("linear", (1.0, 2.0, -3.0, 5.0))
+        c0 = ctx.checksum()
+        ctx.iterate(10)
+        assert ctx.checksum() == c0
+        assert ctx.residual() == 0.0
