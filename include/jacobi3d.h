@@ -221,6 +221,14 @@ J3D_API int jacobi3d_profile_read(jacobi3d_t *ctx, double *total_ms, int64_t *la
  * cross-GPU exchange and its waits are skipped (results become invalid). */
 J3D_API int jacobi3d_set_skip_exchange(jacobi3d_t *ctx, int skip);
 
+/* Self-test of the stencil's division by 7: on the
+ * current CUDA device, compare the kernel's correctly rounded s/7 with the
+ * IEEE division routine (__ddiv_rn) for n generated inputs (random finite bit
+ * patterns incl. subnormals, [0,7), dyadic integers, near-subnormal sums).
+ * *mismatches = number of differing results; example[3] (may be NULL) =
+ * first failing s, kernel result, IEEE result. */
+J3D_API int jacobi3d_div7_selftest(uint64_t n, uint64_t seed, uint64_t *mismatches, double *example);
+
 /* Free everything.  NULL-safe.  Collective when n_gpus > 1. */
 J3D_API int jacobi3d_destroy(jacobi3d_t *ctx);
 

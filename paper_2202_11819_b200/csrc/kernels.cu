@@ -73,6 +73,19 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uin
         : "memory");
 }
 
+// Descriptor loads on rare paths: volatile so the compiler cannot hoist
+// them out of the plane loop (which would pin ~36 registers for the six
+// FaceRefs in the hot loop).
+__device__ __forceinline__ FaceRef load_face(const FaceRef* f) {
+    FaceRef r;
+    uint64_t p;
+    asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(p) : "l"(f));
+    asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(r.sa) : "l"(reinterpret_cast<const char*>(f) + 8));
+    asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(r.sb) : "l"(reinterpret_cast<const char*>(f) + 16));
+    r.p = reinterpret_cast<double*>(p);
+    return r;
+}
+
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     uint64_t z = x + 0x9E3779B97F4A7C15ULL;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -80,201 +93,352 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     return z ^ (z >> 31);
 }
 
-// The update itself: SPEC.md L388, summed left to right, IEEE division.
-__device__ __forceinline__ double jacobi7(double c, double xm, double xp, double ym, double yp, double zm, double zp) {
+// Correctly rounded s / 7 (IEEE round-to-nearest-even) without the generic
+// division routine (whose slow path is a CALL that costs the stencil ~20
+// registers).  Normal results: q = RN(s*y) with y = RN(1/7) is a faithful
+// quotient (7y = 1 - 2^-54 exactly, so s*y lies within half an ulp of s/7);
+// the remainder e = s - 7q is then exact in one FMA and RN(q + e*y) =
+// RN(s/7) (Markstein's correction theorem); for exact quotients e == 0 and
+// the result is q.  Subnormal results and zeros (|s| < 7*2^-1022): s is an
+// integer N times 2^-1074 with |N| < 2^55, and RN(s/7) = 2^-1074 * (N/7
+// rounded to nearest -- 7 is odd, so there are no ties), done in integer
+// arithmetic, with the sign of s (so -0/7 = -0).  DESIGN.md "Division"; checked against __ddiv_rn on the GPU by
+// jacobi3d_div7_selftest.
+constexpr double kDiv7Tiny = 0x1.cp-1020;  // 7 * 2^-1022: below it s/7 is subnormal (or s is 0)
+
+// Fast path, valid for |s| >= kDiv7Tiny: three fp64 ops, no branch.
+__device__ __forceinline__ double div7_fast(double s) {
+    const double y = 0x1.2492492492492p-3;  // RN(1/7)
+    const double q = __dmul_rn(s, y);
+    const double e = __fma_rn(-q, 7.0, s);
+    return __fma_rn(e, y, q);  // exact quotients: e == 0 and the result is q
+}
+
+// All s (the stencil calls it only on the rare path, see stencil_tma_kernel).
+__device__ __forceinline__ double div7(double s) {
+    double r = div7_fast(s);
+    if (fabs(s) < kDiv7Tiny) {  // |s/7| < 2^-1022: subnormal quotient (or zero)
+        const long long n = __double2ll_rn(__dmul_rn(__dmul_rn(s, 0x1p537), 0x1p537));  // exact
+        const long long a = n < 0 ? -n : n;
+        long long k = a / 7;
+        if (a - 7 * k >= 4) k += 1;
+        r = copysign(__dmul_rn((double)k, 0x1p-1074), s);  // sign kept for zero results too
+    }
+    return r;
+}
+
+// The update's sum: SPEC.md L388, left to right (no reassociation, no FMA).
+__device__ __forceinline__ double sum7(double c, double xm, double xp, double ym, double yp, double zm, double zp) {
     double s = __dadd_rn(c, xm);
     s = __dadd_rn(s, xp);
     s = __dadd_rn(s, ym);
     s = __dadd_rn(s, yp);
     s = __dadd_rn(s, zm);
-    s = __dadd_rn(s, zp);
-    return __ddiv_rn(s, 7.0);
+    return __dadd_rn(s, zp);
 }
 
 // ------------------------------------------------------------------ stencil
-template <int TX, int TY, int NSTAGE>
-struct StencilShape {
-    static constexpr int NCW = 8;  // consumer warps
-    static constexpr int RPW = TY / NCW;
-    static constexpr int CPL = TX / 64;  // double2 column groups per lane
-    static constexpr int W = TX + 4;     // smem row: x0-2 .. x0+TX+1
-    static constexpr int H = TY + 2;
+// Tile shape: TX cells along x (a warp covers 64 with double2 per lane, CPL
+// column groups), NCW consumer warps each owning RPW rows (TY = NCW*RPW),
+// NSTAGE plane buffers in the TMA ring, MINB CTAs per SM targeted.
+template <int TX_, int NCW_, int RPW_, int NSTAGE_, int MINB_>
+struct Tile {
+    static constexpr int TX = TX_, NCW = NCW_, RPW = RPW_, NSTAGE = NSTAGE_, MINB = MINB_;
+    static constexpr int TY = NCW * RPW;
+    static constexpr int CPL = TX / 64;
+    static constexpr int W = TX + 4;  // smem row: x0-2 .. x0+TX+1 (16-B aligned interior)
+    static constexpr int H = TY + 2;  // y0-1 .. y0+TY
     static constexpr uint32_t TX_BYTES = W * H * 8;
     static constexpr int STAGE_BYTES = (W * H * 8 + 127) / 128 * 128;
-    static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8 + 128;
+    static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8 + 2 * 4 * 8 + 4 * 4 + 128;
     static constexpr int THREADS = 32 * (NCW + 1);
-    static_assert(TY % NCW == 0 && TX % 64 == 0 && W <= 256, "tile shape");
+    static_assert(TX % 64 == 0 && W <= 256 && H <= 256 && NSTAGE >= 3, "tile shape");
 };
 
-template <int TX, int TY, int NSTAGE, bool FACES>
-__global__ void __launch_bounds__(StencilShape<TX, TY, NSTAGE>::THREADS, FACES ? 1 : 2)
+// Rare path (strategy C prologue, "unpack fused into the update"): overwrite
+// the ghost cells of one freshly landed plane stage with the receive-buffer
+// values, restricted to the cells THIS warp will read (its rows' centres for
+// a ghost plane; the -y / +y ghost row next to its rows; its rows' -x / +x
+// ghost columns), so only a __syncwarp is needed afterwards.
+template <class T>
+__device__ __forceinline__ void patch_stage(const StencilDesc* __restrict__ d, double* st, int zz, int x0, int y0,
+                                         int warp, int lane) {
+    constexpr int W = T::W;
+    const int nx = d->nx, ny = d->ny, nz = d->nz;
+    const uint32_t pro = d->pro_mask;
+    const int r0 = warp * T::RPW;
+    if (zz < 0 || zz >= nz) {
+        const int f = zz < 0 ? 4 : 5;
+        if (!(pro & (1u << f))) return;
+        const FaceRef F = d->pro[f];
+        for (int r = 0; r < T::RPW; ++r) {
+            const int y = y0 + r0 + r;
+            if (y >= ny) break;
+            for (int lx = lane; lx < T::TX; lx += 32) {
+                const int x = x0 + lx;
+                if (x < nx) st[(r0 + r + 1) * W + lx + 2] = F.p[x * F.sa + y * F.sb];
+            }
+        }
+        return;
+    }
+    if ((pro & 4u) && y0 == 0 && warp == 0) {
+        const FaceRef F = load_face(&d->pro[2]);
+        for (int lx = lane; lx < T::TX; lx += 32) {
+            const int x = x0 + lx;
+            if (x < nx) st[lx + 2] = F.p[x * F.sa + zz * F.sb];
+        }
+    }
+    if (pro & 8u) {
+        const int gl = ny - y0;  // tile-local row of the +y ghost
+        if (gl <= T::TY && gl - 1 >= r0 && gl - 1 < r0 + T::RPW) {
+            const FaceRef F = load_face(&d->pro[3]);
+            for (int lx = lane; lx < T::TX; lx += 32) {
+                const int x = x0 + lx;
+                if (x < nx) st[(gl + 1) * W + lx + 2] = F.p[x * F.sa + zz * F.sb];
+            }
+        }
+    }
+    if (lane < T::RPW) {
+        const int y = y0 + r0 + lane;
+        if (y < ny) {
+            if ((pro & 1u) && x0 == 0) {
+                const FaceRef F = load_face(&d->pro[0]);
+                st[(r0 + lane + 1) * W + 1] = F.p[y * F.sa + zz * F.sb];
+            }
+            if (pro & 2u) {
+                const int gx = nx - x0;  // tile-local x of the +x ghost
+                if (gx <= T::TX + 1) {
+                    const FaceRef F = load_face(&d->pro[1]);
+                    st[(r0 + lane + 1) * W + gx + 2] = F.p[y * F.sa + zz * F.sb];
+                }
+            }
+        }
+    }
+}
+
+// Rare path (strategy C / direct epilogue, "pack fused into the update"):
+// store the new values of a boundary cell pair to the face destinations.
+__device__ __forceinline__ void epi_store(const StencilDesc* __restrict__ d, int x, int y, int z, double vx, double vy,
+                                       bool has2) {
+    const uint32_t epi = d->epi_mask;
+    const int nx = d->nx, ny = d->ny, nz = d->nz;
+    if ((epi & 1u) && x == 0) { const FaceRef f = load_face(&d->epi[0]); f.p[y * f.sa + z * f.sb] = vx; }
+    if (epi & 2u) {
+        const FaceRef f = load_face(&d->epi[1]);
+        if (x == nx - 1) f.p[y * f.sa + z * f.sb] = vx;
+        else if (has2 && x + 1 == nx - 1) f.p[y * f.sa + z * f.sb] = vy;
+    }
+    if ((epi & 4u) && y == 0) {
+        const FaceRef f = load_face(&d->epi[2]);
+        f.p[x * f.sa + z * f.sb] = vx;
+        if (has2) f.p[(x + 1) * f.sa + z * f.sb] = vy;
+    }
+    if ((epi & 8u) && y == ny - 1) {
+        const FaceRef f = load_face(&d->epi[3]);
+        f.p[x * f.sa + z * f.sb] = vx;
+        if (has2) f.p[(x + 1) * f.sa + z * f.sb] = vy;
+    }
+    if ((epi & 16u) && z == 0) {
+        const FaceRef f = load_face(&d->epi[4]);
+        f.p[x * f.sa + y * f.sb] = vx;
+        if (has2) f.p[(x + 1) * f.sa + y * f.sb] = vy;
+    }
+    if ((epi & 32u) && z == nz - 1) {
+        const FaceRef f = load_face(&d->epi[5]);
+        f.p[x * f.sa + y * f.sb] = vx;
+        if (has2) f.p[(x + 1) * f.sa + y * f.sb] = vy;
+    }
+}
+
+// Work distribution: the producer of each CTA takes items in list order from
+// a global counter (sched[0]), so the items of one z chunk -- in particular
+// y- and x-neighbouring tiles, whose halos overlap -- run at the same time
+// and the overlapping halo rows/columns are served from L2.  A 4-deep item
+// queue in shared memory hands the indices to the consumer warps.  The last
+// CTA to finish resets the counter (sched[1] counts finished CTAs), so the
+// kernel is reusable and graph-capturable without a memset.
+template <class T>
+__global__ void __launch_bounds__(T::THREADS, T::MINB)
     stencil_tma_kernel(const StencilDesc* __restrict__ descs, const CUtensorMap* __restrict__ tmaps,
-                       const WorkItem* __restrict__ items, int n_items, int parity) {
-    using S = StencilShape<TX, TY, NSTAGE>;
-    constexpr int NCW = S::NCW, RPW = S::RPW, CPL = S::CPL, W = S::W;
-    extern __shared__ unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NSTAGE * S::STAGE_BYTES);
+                       const WorkItem* __restrict__ items, int n_items, int parity, int flags,
+                       unsigned int* __restrict__ sched) {
+    constexpr int NCW = T::NCW, RPW = T::RPW, CPL = T::CPL, W = T::W, NSTAGE = T::NSTAGE, IQ = 4;
+    // The kernel has no static shared memory, so the dynamic window starts at
+    // shared offset 0 (1024-B aligned); indexing the __shared__ array directly
+    // keeps the state space known to the compiler (LDS, not generic LD).
+    extern __shared__ __align__(1024) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NSTAGE * T::STAGE_BYTES);
     uint64_t* empty = full + NSTAGE;
+    uint64_t* qfull = empty + NSTAGE;
+    uint64_t* qempty = qfull + IQ;
+    volatile int* queue = reinterpret_cast<volatile int*>(qempty + IQ);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool faces = flags & 1;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < NSTAGE; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NCW);
+        for (int i = 0; i < NSTAGE; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], NCW);
+        }
+        for (int i = 0; i < IQ; ++i) {
+            mbar_init(&qfull[i], 1);
+            mbar_init(&qempty[i], NCW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
-    if (warp == NCW) {  // ---------------- producer warp: TMA plane loads
+    if (warp == NCW) {  // ---------------- producer warp: item scheduling + TMA plane loads
         if (lane == 0) {
-            int s = 0;
-            uint32_t ph = 0;
-            for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+            int s = 0, qs = 0;
+            uint32_t ph = 0, qph = 0;
+            for (;;) {
+                int it = (int)atomicAdd(&sched[0], 1u);
+                if (it >= n_items) it = -1;
+                mbar_wait(&qempty[qs], qph ^ 1);
+                queue[qs] = it;
+                mbar_arrive(&qfull[qs]);
+                if (++qs == IQ) { qs = 0; qph ^= 1; }
+                if (it < 0) break;
                 const WorkItem w = items[it];
                 const CUtensorMap* tm = tmaps + (2 * w.blk + parity);
                 tmap_acquire(tm);
-                const int c0 = XOFF + w.tx * TX - 2, c1 = w.ty * TY;
+                const int c0 = XOFF + w.tx * T::TX - 2, c1 = w.ty * T::TY;
                 for (int z = w.z0 - 1; z <= w.z1; ++z) {
                     mbar_wait(&empty[s], ph ^ 1);
-                    mbar_expect_tx(&full[s], S::TX_BYTES);
-                    tma_load_3d(smem + s * S::STAGE_BYTES, tm, &full[s], c0, c1, z + 1);
+                    mbar_expect_tx(&full[s], T::TX_BYTES);
+                    tma_load_3d(smem + s * T::STAGE_BYTES, tm, &full[s], c0, c1, z + 1);
                     if (++s == NSTAGE) { s = 0; ph ^= 1; }
                 }
+            }
+            __threadfence();
+            if (atomicAdd(&sched[1], 1u) == gridDim.x - 1) {  // every CTA has taken its last item
+                sched[0] = 0;
+                sched[1] = 0;
+                __threadfence();
             }
         }
         return;
     }
 
     // ---------------- consumer warps
-    int s = 0;
-    uint32_t ph = 0;
+    uint64_t store_policy = 0;
+    const bool hint = flags & 2;
+    if (hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(store_policy));
+    int s = 0, qs = 0;
+    uint32_t ph = 0, qph = 0;
+    auto stage = [&](int i) -> double* { return reinterpret_cast<double*>(smem + i * T::STAGE_BYTES); };
     auto advance = [&]() { if (++s == NSTAGE) { s = 0; ph ^= 1; } };
-    auto stage = [&](int i) { return reinterpret_cast<const double*>(smem + i * S::STAGE_BYTES); };
 
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (;;) {
+        mbar_wait(&qfull[qs], qph);
+        const int it = queue[qs];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&qempty[qs]);
+        if (++qs == IQ) { qs = 0; qph ^= 1; }
+        if (it < 0) break;
+
         const WorkItem w = items[it];
         const StencilDesc* d = descs + (2 * w.blk + parity);
         const int nx = d->nx, ny = d->ny, nz = d->nz;
         const int64_t pitch = d->pitch, zs = d->zs;
-        double* __restrict__ out = d->out;
-        const uint32_t epi = FACES ? d->epi_mask : 0u, pro = FACES ? d->pro_mask : 0u;
-        const int x0 = w.tx * TX, y0 = w.ty * TY;
-        const bool edge_xy = FACES && (epi | pro) &&
-                             (x0 == 0 || x0 + TX >= nx - 1 || y0 == 0 || y0 + TY >= ny);
+        const int x0 = w.tx * T::TX, y0 = w.ty * T::TY;
+        const int xl = x0 + 2 * lane, yl = y0 + warp * RPW;  // this thread's first cell (c = 0, r = 0)
+        double* obase = d->out + (int64_t)(yl + 1) * pitch + XOFF + xl;
+        const uint32_t pro = faces ? d->pro_mask : 0u;
+        const uint32_t epi = faces ? d->epi_mask : 0u;
+        const bool edge_xy = x0 == 0 || x0 + T::TX + 1 >= nx || y0 == 0 || y0 + T::TY >= ny;
+        const bool whole = x0 + T::TX <= nx && y0 + T::TY <= ny;  // no cell of the tile is outside the block
+        const int sbase = (warp * RPW + 1) * W + 2 * lane + 2;  // smem offset of cell (r = 0, c = 0)
 
-        double2 prev[RPW][CPL], cur[RPW][CPL], nxt[RPW][CPL];
+        // wait for the stage of plane zz, patch its ghosts (fused prologue) if needed
+        auto acquire = [&](int zz) {
+            mbar_wait(&full[s], ph);
+            if (pro && (edge_xy || zz < 0 || zz >= nz)) {
+                patch_stage<T>(d, stage(s), zz, x0, y0, warp, lane);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+            }
+        };
         auto read_centres = [&](const double* st, double2 (&v)[RPW][CPL]) {
 #pragma unroll
             for (int r = 0; r < RPW; ++r)
 #pragma unroll
-                for (int c = 0; c < CPL; ++c)
-                    v[r][c] = *reinterpret_cast<const double2*>(st + (warp * RPW + r + 1) * W + 64 * c + 2 * lane + 2);
-        };
-        // face (z-plane) prologue: centre values of a ghost plane from a receive buffer
-        auto read_face_plane = [&](const FaceRef& f, double2 (&v)[RPW][CPL]) {
-#pragma unroll
-            for (int r = 0; r < RPW; ++r) {
-                const int y = y0 + warp * RPW + r;
-#pragma unroll
-                for (int c = 0; c < CPL; ++c) {
-                    const int x = x0 + 64 * c + 2 * lane;
-                    if (y < ny && x < nx) {
-                        v[r][c].x = f.p[x * f.sa + y * f.sb];
-                        if (x + 1 < nx) v[r][c].y = f.p[(x + 1) * f.sa + y * f.sb];
-                    }
-                }
-            }
+                for (int c = 0; c < CPL; ++c) v[r][c] = *reinterpret_cast<const double2*>(st + sbase + r * W + 64 * c);
         };
 
-        // plane z0-1: only its centre values are needed (as -z neighbours)
-        mbar_wait(&full[s], ph);
-        read_centres(stage(s), prev);
+        double2 A[RPW][CPL], B[RPW][CPL], C[RPW][CPL];
+        acquire(w.z0 - 1);
+        read_centres(stage(s), A);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         advance();
-        if (FACES && w.z0 == 0 && (pro & (1u << 4))) read_face_plane(d->pro[4], prev);
-        // plane z0
-        mbar_wait(&full[s], ph);
-        read_centres(stage(s), cur);
+        acquire(w.z0);
+        read_centres(stage(s), B);
         int scur = s;
         advance();
 
-        for (int z = w.z0; z < w.z1; ++z) {
-            mbar_wait(&full[s], ph);
-            read_centres(stage(s), nxt);
-            if (FACES && z + 1 == nz && (pro & (1u << 5))) read_face_plane(d->pro[5], nxt);
-            const double* st = stage(scur);
-            const bool face_here = FACES && (epi | pro) && (edge_xy || z == 0 || z == nz - 1);
+        // One output plane z from (P = z-1, Q = z, N <- z+1), called with the
+        // three register sets in rotated roles so no register moves are needed.
+        // Hot part: no branches but the store predicates.  Rare part (a tiny
+        // sum needing the subnormal-exact division, or a plane with fused-
+        // epilogue faces): recompute the cells from the same inputs and store
+        // again / store the face values.
+        auto plane = [&](int z, const double2 (&P)[RPW][CPL], const double2 (&Q)[RPW][CPL],
+                         double2 (&N)[RPW][CPL]) {
+            acquire(z + 1);
+            read_centres(stage(s), N);
+            const double* st = stage(scur) + sbase;
+            double* op = obase + (int64_t)(z + 1) * zs;
+            bool tiny = false;
 #pragma unroll
             for (int r = 0; r < RPW; ++r) {
-                const int ly = warp * RPW + r;
-                const int y = y0 + ly;
-                if (y >= ny) continue;
-                double* orow = out + (int64_t)(z + 1) * zs + (int64_t)(y + 1) * pitch + XOFF;
 #pragma unroll
                 for (int c = 0; c < CPL; ++c) {
-                    const int lx = 64 * c + 2 * lane;
-                    const int x = x0 + lx;
-                    if (x >= nx) continue;
-                    const double* p = st + (ly + 1) * W + lx + 2;
-                    double2 cc = cur[r][c];
-                    double L = p[-1];
-                    double R = p[2];
-                    double2 ym = *reinterpret_cast<const double2*>(p - W);
-                    double2 yp = *reinterpret_cast<const double2*>(p + W);
-                    const double2 zm = prev[r][c], zp = nxt[r][c];
-                    const bool has2 = x + 1 < nx;
-                    if (FACES && face_here && pro) {  // prologue: ghosts from receive buffers
-                        if ((pro & 1u) && x == 0) { const FaceRef f = d->pro[0]; L = f.p[y * f.sa + z * f.sb]; }
-                        if (pro & 2u) {
-                            const FaceRef f = d->pro[1];
-                            if (x + 1 == nx) cc.y = f.p[y * f.sa + z * f.sb];
-                            else if (x + 2 == nx) R = f.p[y * f.sa + z * f.sb];
-                        }
-                        if ((pro & 4u) && y == 0) {
-                            const FaceRef f = d->pro[2];
-                            ym.x = f.p[x * f.sa + z * f.sb];
-                            if (has2) ym.y = f.p[(x + 1) * f.sa + z * f.sb];
-                        }
-                        if ((pro & 8u) && y == ny - 1) {
-                            const FaceRef f = d->pro[3];
-                            yp.x = f.p[x * f.sa + z * f.sb];
-                            if (has2) yp.y = f.p[(x + 1) * f.sa + z * f.sb];
-                        }
+                    const double* p = st + r * W + 64 * c;
+                    const double2 cc = Q[r][c];
+                    const double2 ym = *reinterpret_cast<const double2*>(p - W);
+                    const double2 yp = *reinterpret_cast<const double2*>(p + W);
+                    const double s0 = sum7(cc.x, p[-1], cc.y, ym.x, yp.x, P[r][c].x, N[r][c].x);
+                    const double s1 = sum7(cc.y, cc.x, p[2], ym.y, yp.y, P[r][c].y, N[r][c].y);
+                    tiny |= (fabs(s0) < kDiv7Tiny) | (fabs(s1) < kDiv7Tiny);
+                    const double vx = div7_fast(s0), vy = div7_fast(s1);
+                    double* o = op + r * pitch + 64 * c;
+                    const int x = xl + 64 * c, y = yl + r;
+                    if (whole || (y < ny && x + 1 < nx)) {
+                        if (hint)
+                            asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(o), "d"(vx),
+                                         "d"(vy), "l"(store_policy)
+                                         : "memory");
+                        else
+                            *reinterpret_cast<double2*>(o) = make_double2(vx, vy);
+                    } else if (y < ny && x < nx) {
+                        o[0] = vx;
                     }
-                    const double vx = jacobi7(cc.x, L, cc.y, ym.x, yp.x, zm.x, zp.x);
-                    const double vy = jacobi7(cc.y, cc.x, R, ym.y, yp.y, zm.y, zp.y);
-                    if (has2) *reinterpret_cast<double2*>(orow + x) = make_double2(vx, vy);
-                    else orow[x] = vx;
-                    if (FACES && face_here && epi) {  // epilogue: new boundary layer -> face destinations
-                        if ((epi & 1u) && x == 0) { const FaceRef f = d->epi[0]; f.p[y * f.sa + z * f.sb] = vx; }
-                        if (epi & 2u) {
-                            const FaceRef f = d->epi[1];
-                            if (x == nx - 1) f.p[y * f.sa + z * f.sb] = vx;
-                            else if (x + 1 == nx - 1) f.p[y * f.sa + z * f.sb] = vy;
-                        }
-                        if ((epi & 4u) && y == 0) {
-                            const FaceRef f = d->epi[2];
-                            f.p[x * f.sa + z * f.sb] = vx;
-                            if (has2) f.p[(x + 1) * f.sa + z * f.sb] = vy;
-                        }
-                        if ((epi & 8u) && y == ny - 1) {
-                            const FaceRef f = d->epi[3];
-                            f.p[x * f.sa + z * f.sb] = vx;
-                            if (has2) f.p[(x + 1) * f.sa + z * f.sb] = vy;
-                        }
-                        if ((epi & 16u) && z == 0) {
-                            const FaceRef f = d->epi[4];
-                            f.p[x * f.sa + y * f.sb] = vx;
-                            if (has2) f.p[(x + 1) * f.sa + y * f.sb] = vy;
-                        }
-                        if ((epi & 32u) && z == nz - 1) {
-                            const FaceRef f = d->epi[5];
-                            f.p[x * f.sa + y * f.sb] = vx;
-                            if (has2) f.p[(x + 1) * f.sa + y * f.sb] = vy;
-                        }
+                }
+            }
+            const bool face_plane = epi && (edge_xy || z == 0 || z == nz - 1);
+            if (tiny || face_plane) {
+#pragma unroll
+                for (int r = 0; r < RPW; ++r) {
+#pragma unroll
+                    for (int c = 0; c < CPL; ++c) {
+                        const int x = xl + 64 * c, y = yl + r;
+                        if (y >= ny || x >= nx) continue;
+                        const bool has2 = x + 1 < nx;
+                        const bool onb = face_plane && (x == 0 || x + 2 >= nx || y == 0 || y == ny - 1 || z == 0 ||
+                                                        z == nz - 1);
+                        if (!tiny && !onb) continue;
+                        const double* p = st + r * W + 64 * c;
+                        const double2 cc = Q[r][c];
+                        const double2 ym = *reinterpret_cast<const double2*>(p - W);
+                        const double2 yp = *reinterpret_cast<const double2*>(p + W);
+                        const double vx = div7(sum7(cc.x, p[-1], cc.y, ym.x, yp.x, P[r][c].x, N[r][c].x));
+                        const double vy = div7(sum7(cc.y, cc.x, p[2], ym.y, yp.y, P[r][c].y, N[r][c].y));
+                        double* o = op + r * pitch + 64 * c;
+                        o[0] = vx;
+                        if (has2) o[1] = vy;
+                        if (onb) epi_store(d, x, y, z, vx, vy, has2);
                     }
                 }
             }
@@ -282,13 +446,15 @@ __global__ void __launch_bounds__(StencilShape<TX, TY, NSTAGE>::THREADS, FACES ?
             if (lane == 0) mbar_arrive(&empty[scur]);
             scur = s;
             advance();
-#pragma unroll
-            for (int r = 0; r < RPW; ++r)
-#pragma unroll
-                for (int c = 0; c < CPL; ++c) {
-                    prev[r][c] = cur[r][c];
-                    cur[r][c] = nxt[r][c];
-                }
+        };
+
+        for (int z = w.z0;;) {
+            if (z >= w.z1) break;
+            plane(z++, A, B, C);
+            if (z >= w.z1) break;
+            plane(z++, B, C, A);
+            if (z >= w.z1) break;
+            plane(z++, C, A, B);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[scur]);  // plane z1
@@ -382,48 +548,115 @@ __global__ void __launch_bounds__(256) residual_kernel(const BlockGeom* __restri
     if ((threadIdx.x & 31) == 0) atomicMax(acc, (unsigned long long)__double_as_longlong(m));
 }
 
+// ------------------------------------------------------------------ division self-test
+// Compares div7 with the IEEE division routine on n inputs drawn from
+// splitmix64: mode 0 = random bit patterns (all finite doubles, including
+// subnormals), 1 = uniform in [0,7) (the workloads' range), 2 = small
+// integers times 2^-k (exact / tie-prone quotients), 3 = |s| near the
+// subnormal boundary.
+__global__ void div7_selftest_kernel(uint64_t n, uint64_t seed, unsigned long long* bad, double* example) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t h = splitmix64(seed ^ (i * 0x9E3779B97F4A7C15ULL));
+        const int mode = (int)(i & 3);
+        double s;
+        if (mode == 0) {
+            s = __longlong_as_double((long long)h);
+            if (isnan(s) || isinf(s)) continue;
+        } else if (mode == 1) {
+            s = (double)(h >> 11) * 0x1p-53 * 7.0;
+        } else if (mode == 2) {
+            s = ldexp((double)((long long)(h >> 40) - (1LL << 23)), -(int)((h >> 8) & 63));
+        } else {
+            s = ldexp((double)(h >> 11) * 0x1p-53 + 0.5, -1016 - (int)((h >> 4) & 63));
+            if (h & 1) s = -s;
+        }
+        const double a = div7(s), b = __ddiv_rn(s, 7.0);
+        if (__double_as_longlong(a) != __double_as_longlong(b)) {
+            if (atomicAdd(bad, 1ULL) == 0) { example[0] = s; example[1] = a; example[2] = b; }
+        }
+    }
+}
+
+cudaError_t launch_div7_selftest(uint64_t n, uint64_t seed, unsigned long long* bad, double* example, int sms,
+                                 cudaStream_t st) {
+    div7_selftest_kernel<<<sms * 8, 256, 0, st>>>(n, seed, bad, example);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ host launchers
-template <int TX, int TY, int NSTAGE, bool FACES>
-static cudaError_t launch_stencil_t(const StencilLaunch& L, cudaStream_t st) {
-    using S = StencilShape<TX, TY, NSTAGE>;
-    auto kern = stencil_tma_kernel<TX, TY, NSTAGE, FACES>;
-    static bool attr_set = false;  // per instantiation
+// Tile configurations selectable at run time (kind index):
+//          TX  NCW RPW NSTAGE MINB      tile     CTAs/SM (smem)
+#define J3D_TILES(X)                                                        \
+    X(0, 128, 8, 2, 4, 2)   /* 128x16, 4 x 19 KB stages                */ \
+    X(1, 64, 8, 2, 4, 2)    /* 64x16, 4 x 9.8 KB                       */ \
+    X(2, 64, 8, 2, 6, 2)    /* 64x16, 6 stages                         */ \
+    X(3, 128, 8, 2, 8, 1)   /* 128x16, 8 stages, 1 CTA/SM              */ \
+    X(4, 128, 8, 1, 6, 2)   /* 128x8, 6 x 10.5 KB                      */ \
+    X(5, 64, 16, 2, 6, 1)   /* 64x32, 16 consumer warps                */ \
+    X(6, 64, 16, 1, 6, 2)   /* 64x16, 16 consumer warps                */ \
+    X(7, 64, 8, 1, 6, 3)    /* 64x8, 3 CTAs/SM                         */ \
+    X(8, 64, 8, 2, 4, 3)    /* 64x16, 3 CTAs/SM                        */ \
+    X(9, 128, 16, 1, 4, 1)  /* 128x16, 16 consumer warps, 1 CTA/SM     */ \
+    X(10, 128, 8, 1, 8, 2)  /* 128x8, 8 stages                         */ \
+    X(11, 128, 15, 2, 4, 1) /* 128x30, 15 consumer warps, 4 x 34 KB    */ \
+    X(12, 128, 11, 2, 6, 1) /* 128x22, 11 consumer warps, 6 x 25 KB    */
+
+template <class T>
+static cudaError_t launch_t(const StencilLaunch& L, cudaStream_t st) {
+    static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM_BYTES);
+        cudaError_t e = cudaFuncSetAttribute(stencil_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             T::SMEM_BYTES);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     if (L.n_items <= 0) return cudaSuccess;
-    kern<<<L.grid, S::THREADS, S::SMEM_BYTES, st>>>(L.descs, L.tmaps, L.items, L.n_items, L.parity);
+    stencil_tma_kernel<T><<<L.grid, T::THREADS, T::SMEM_BYTES, st>>>(L.descs, L.tmaps, L.items, L.n_items, L.parity,
+                                                                     (L.faces ? 1 : 0) | (L.store_hint ? 2 : 0),
+                                                                     L.sched);
     return cudaGetLastError();
 }
 
-template <int TX, int TY, int NSTAGE, bool FACES>
-static cudaError_t occupancy_t(int* blocks) {
-    using S = StencilShape<TX, TY, NSTAGE>;
-    auto kern = stencil_tma_kernel<TX, TY, NSTAGE, FACES>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM_BYTES);
+template <class T>
+static cudaError_t occ_t(int* blocks) {
+    cudaError_t e = cudaFuncSetAttribute(stencil_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         T::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, kern, S::THREADS, S::SMEM_BYTES);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, stencil_tma_kernel<T>, T::THREADS, T::SMEM_BYTES);
 }
 
-// Tile configurations (TX, TY, NSTAGE).  Kind 0: wide blocks, kind 1: narrow.
-#define J3D_TILE0 128, 16, 4
-#define J3D_TILE1 64, 16, 4
+#define J3D_TYPE(k, tx, ncw, rpw, ns, mb) Tile<tx, ncw, rpw, ns, mb>
+
+int num_tile_kinds() { return 13; }
 
 TileShape tile_shape(int kind) {
-    if (kind == 0) return TileShape{128, 16};
-    return TileShape{64, 16};
+    switch (kind) {
+#define X(k, tx, ncw, rpw, ns, mb) \
+    case k: return TileShape{tx, ncw * rpw};
+        J3D_TILES(X)
+#undef X
+    }
+    return TileShape{0, 0};
 }
 
 cudaError_t launch_stencil(const StencilLaunch& L, cudaStream_t st) {
-    if (L.kind == 0) return L.faces ? launch_stencil_t<J3D_TILE0, true>(L, st) : launch_stencil_t<J3D_TILE0, false>(L, st);
-    return L.faces ? launch_stencil_t<J3D_TILE1, true>(L, st) : launch_stencil_t<J3D_TILE1, false>(L, st);
+    switch (L.kind) {
+#define X(k, tx, ncw, rpw, ns, mb) \
+    case k: return launch_t<J3D_TYPE(k, tx, ncw, rpw, ns, mb)>(L, st);
+        J3D_TILES(X)
+#undef X
+    }
+    return cudaErrorInvalidValue;
 }
 
-cudaError_t stencil_occupancy(int kind, bool faces, int* blocks_per_sm) {
-    if (kind == 0) return faces ? occupancy_t<J3D_TILE0, true>(blocks_per_sm) : occupancy_t<J3D_TILE0, false>(blocks_per_sm);
-    return faces ? occupancy_t<J3D_TILE1, true>(blocks_per_sm) : occupancy_t<J3D_TILE1, false>(blocks_per_sm);
+cudaError_t stencil_occupancy(int kind, bool, int* blocks_per_sm) {
+    switch (kind) {
+#define X(k, tx, ncw, rpw, ns, mb) \
+    case k: return occ_t<J3D_TYPE(k, tx, ncw, rpw, ns, mb)>(blocks_per_sm);
+        J3D_TILES(X)
+#undef X
+    }
+    return cudaErrorInvalidValue;
 }
 
 int stencil_box_w(int kind) { return tile_shape(kind).tx + 4; }

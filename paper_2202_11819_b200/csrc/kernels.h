@@ -20,15 +20,20 @@ struct StencilLaunch {
     int n_items;
     int parity;  // input buffer parity
     int grid;    // persistent CTAs
-    int kind;    // tile kind (0: 128x16, 1: 64x16)
+    int kind;    // tile configuration (kernels.cu J3D_TILES)
     bool faces;  // any prologue/epilogue faces in this launch
+    bool store_hint;         // L2 evict_first policy on the output stores
+    unsigned int* sched;     // device [2] scheduler counters (zero on entry; reset by the kernel)
 };
 
+int num_tile_kinds();
 TileShape tile_shape(int kind);
 int stencil_box_w(int kind);
 int stencil_box_h(int kind);
 cudaError_t launch_stencil(const StencilLaunch& L, cudaStream_t st);
 cudaError_t stencil_occupancy(int kind, bool faces, int* blocks_per_sm);
+cudaError_t launch_div7_selftest(uint64_t n, uint64_t seed, unsigned long long* bad, double* example, int sms,
+                                 cudaStream_t st);
 cudaError_t launch_copy_faces(const CopyDesc* d, int per_group, int groups, int64_t max_cells, cudaStream_t st);
 cudaError_t launch_init(const BlockGeom* g, int nblocks, int max_nx, int64_t max_rows, int kind, const double* p,
                         uint64_t seed, double boundary, int64_t gx, int64_t gy, int64_t gz, cudaStream_t st);

@@ -82,6 +82,7 @@ def _load():
         "jacobi3d_profile_read": [P, ctypes.POINTER(D), ctypes.POINTER(I64), ctypes.POINTER(D)],
         "jacobi3d_set_skip_exchange": [P, ctypes.c_int],
         "jacobi3d_destroy": [P],
+        "jacobi3d_div7_selftest": [U64, U64, ctypes.POINTER(U64), P],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -126,6 +127,14 @@ def nccl_unique_id() -> bytes:
     buf = (ctypes.c_uint8 * 128)()
     _ck(lib.jacobi3d_nccl_unique_id(buf))
     return bytes(buf)
+
+
+def div7_selftest(n: int, seed: int = 1):
+    """Kernel division by 7 vs the IEEE routine on the current device."""
+    bad = ctypes.c_uint64()
+    ex = (ctypes.c_double * 3)()
+    _ck(lib.jacobi3d_div7_selftest(n, seed, ctypes.byref(bad), ex))
+    return bad.value, tuple(ex)
 
 
 class Jacobi3D:

@@ -1,0 +1,41 @@
+"""Summarise an ncu --set full report (raw page) into the metrics we track."""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram__bytes.sum.per_second",
+        "lts__t_sector_hit_rate.pct", "lts__t_bytes.sum", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+        "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem", "launch__grid_size",
+        "launch__block_size", "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+        "smsp__inst_executed.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+        "sm__cycles_elapsed.avg.per_second", "dram__cycles_elapsed.avg.per_second"]
+
+
+def summary(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        d = {}
+        for w in WANT:
+            if w in hdr:
+                i = hdr.index(w)
+                d[w] = (r[i], units[i])
+        if "Kernel Name" in hdr:
+            d["kernel"] = r[hdr.index("Kernel Name")][:80]
+        res.append(d)
+    return res
+
+
+if __name__ == "__main__":
+    for rep in sys.argv[1:]:
+        for d in summary(rep):
+            print(rep)
+            for k, v in d.items():
+                print(f"  {k:64s} {v}")

@@ -167,3 +167,25 @@ def test_get_region_matches_get_block():
         full = ctx.get_block(1)
         reg = ctx.get_region(1, (5, 3, 2), (11, 7, 4))
         assert_bitwise(reg, full[2:6, 3:10, 5:16], "region")
+
+
+def test_div7_matches_ieee_division():
+    """The stencil's s/7 (Markstein-corrected reciprocal + exact integer path
+    for subnormal quotients) is bitwise the IEEE
+    round-to-nearest division on 2^27 inputs per seed, including random bit
+    patterns, subnormals and exact/tie-prone dyadic values."""
+    from paper_2202_11819_b200.jacobi3d import div7_selftest
+
+    for seed in (1, 2):
+        bad, ex = div7_selftest(1 << 27, seed)
+        assert bad == 0, ex
+
+
+@pytest.mark.parametrize("scale_exp", [-1060, -1030, -1074 + 60])
+def test_subnormal_values(scale_exp):
+    """Sums whose quotient is subnormal take the stencil's exact rare path
+    (DESIGN.md "Division"); mixed signs and -0.0 included, Dirichlet 0."""
+    U0 = uniform_field(40, 24, 16, seed=11, boundary=0.0) * 2.0 ** scale_exp
+    U0[5:9, 5:9, 5:9] = -0.0
+    for v in ("direct", "unfused", "C"):
+        _case((40, 24, 16), 4, v, "batched", False, 9, boundary=0.0, field=U0)
