@@ -593,14 +593,19 @@ void cross_gpu_exchange(jacobi3d* c, int par, int slot) {
     p2p_sync(c, slot);
 }
 
-// Full halo refresh of buffer parity `par`: pack, exchange, unpack, batched on main.
+// Full halo refresh of buffer parity `par`: pack, exchange, unpack, batched on
+// main.  With P2P peers it starts with an epoch barrier (slots 4/5): a peer's
+// NVLink stores into our receive buffers may only begin once we have finished
+// every earlier use of them (the caller's state change, e.g. init or
+// set_block, or the last iteration of a previous run).
 void refresh(jacobi3d* c, int par) {
-    copies(c, c->d_pack, par, -1, 0, true, c->main);
-    const int slot = 2 + (int)(c->refresh_count & 1);
+    const int rc = (int)(c->refresh_count & 1);
     c->refresh_count++;
+    if (c->n_gpus > 1) p2p_sync(c, 4 + rc);
+    copies(c, c->d_pack, par, -1, 0, true, c->main);
     if (c->n_gpus > 1) {
         nccl_exchange(c, par);
-        p2p_sync(c, slot);
+        p2p_sync(c, 2 + rc);
     }
     copies(c, c->d_unpack, par, -1, 0, true, c->main);
 }
@@ -878,6 +883,9 @@ int jacobi3d_create(const jacobi3d_config* cfg, const uint8_t* nccl_uid, jacobi3
         build_layout(c);
         CK(cudaMalloc(&c->arena, (size_t)c->arena_bytes));
         CK(cudaMemset(c->arena, 0, 4096));
+        // face buffers start zeroed; done here, before any peer can map the
+        // arena, so it can never race with a peer's NVLink stores
+        CK(cudaMemset(c->arena + c->off_faces, 0, (size_t)(c->arena_bytes - c->off_faces)));
         CK(cudaMalloc(&c->d_descs, sizeof(StencilDesc) * 2 * c->n_local));
         CK(cudaMalloc(&c->d_tmaps, sizeof(CUtensorMap) * 2 * c->n_local));
         CK(cudaMalloc(&c->d_pack, sizeof(CopyDesc) * 12 * c->n_local));
@@ -992,8 +1000,6 @@ int jacobi3d_init(jacobi3d_t* c, int kind, const double* p, uint64_t seed) {
         CK(launch_init(c->d_geom, c->n_local, (int)c->nx, (c->ny + 2) * (c->nz + 2), kind, pp, seed,
                        c->cfg.boundary, c->cfg.gx, c->cfg.gy, c->cfg.gz, c->main));
         count_launch(c, -1);
-        // zero face buffers so that stale data can never masquerade as a halo
-        CK(cudaMemsetAsync(c->arena + c->off_faces, 0, (size_t)(c->arena_bytes - c->off_faces), c->main));
         c->iter = 0;
         c->iter_since_set = 0;
         c->halos_stale = false;

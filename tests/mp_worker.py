@@ -1,0 +1,92 @@
+"""Multi-GPU parity worker (one process per GPU, launched by torchrun from
+tests/test_gpu_multi.py).  Every rank runs the same cases collectively; each
+rank checks its own blocks bit for bit against the CPU oracle (computed
+locally on the same seeded input) and all ranks check the global checksum and
+residual.  Prints "MP OK <n>" on success, raises otherwise.
+"""
+import itertools
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from oracle import core  # noqa: E402
+from paper_2202_11819_b200 import dist as jdist  # noqa: E402
+
+
+def run_case(grid, odf, variant, launch, graph, exchange, n, kind, seed):
+    ctx = jdist.create(grid, odf=odf, variant=variant, launch=launch, graph=graph, exchange=exchange)
+    try:
+        ctx.init(kind, seed=seed)
+        ctx.iterate(n)
+        ctx.synchronize()
+        got = ctx.gather_local()
+        ck = ctx.checksum()
+        res = ctx.residual() if n > 0 else None
+        U0 = core.init(*grid, core.INIT_HASH if kind == "hash" else core.INIT_DEFAULT, seed=seed)
+        want, prev = core.run_pair(U0, n) if n > 0 else (U0, None)
+        W = core.owned(want)
+        mask = ~np.isnan(got)
+        tag = f"rank {dist.get_rank()} {grid} odf={odf} {variant}/{launch}/graph={graph}/{exchange} {kind}"
+        assert mask.any(), tag
+        badm = mask & (got.view(np.uint64) != np.ascontiguousarray(W).view(np.uint64))
+        if badm.any():
+            idx = np.argwhere(badm)
+            zs_ = sorted(set(idx[:, 0].tolist()))
+            raise AssertionError(f"{tag}: {int(badm.sum())} cells differ; z planes {zs_[:8]}..{zs_[-4:]} "
+                                 f"y range {idx[:,1].min()}-{idx[:,1].max()} x range {idx[:,2].min()}-{idx[:,2].max()}; "
+                                 f"first {idx[0].tolist()} got {got[tuple(idx[0])]!r} want {W[tuple(idx[0])]!r}")
+        assert ck == core.checksum(want), tag
+        if n > 0:
+            assert np.float64(res).tobytes() == np.float64(core.residual(want, prev)).tobytes(), tag
+        st = ctx.stats()
+        return st
+    finally:
+        ctx.close()
+
+
+def main():
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    world = dist.get_world_size()
+    which = sys.argv[1] if len(sys.argv) > 1 else "quick"
+    cases = []
+    grids = {2: (48, 40, 64), 4: (48, 64, 64)}
+    g = grids.get(world, (64, 64, 64))
+    for exchange, variant, launch, graph in itertools.product(["nccl", "p2p"], ["direct", "C", "unfused", "B"],
+                                                               ["batched", "per_block"], [False, True]):
+        if which == "quick" and (launch, graph) == ("per_block", True):
+            continue
+        cases.append((g, 4, variant, launch, graph, exchange, 9, "hash", 3))
+    cases.append((g, 1, "direct", "batched", False, "p2p", 12, "default", 0))
+    cases.append((g, 1, "unfused", "batched", False, "nccl", 12, "default", 0))
+    cases.append(((45, 34, 44), 2, "direct", "batched", False, "p2p", 7, "hash", 1))
+    cases.append(((45, 34, 44), 2, "C", "per_block", False, "nccl", 7, "hash", 1))
+    if which == "debug":
+        cases = [((16, 8, 16), 1, "direct", "batched", False, "p2p", n_, "hash", 3) for n_ in (0, 1, 2, 3)]
+        cases += [((16, 8, 16), 1, v, "batched", False, "p2p", 2, "hash", 3) for v in ("unfused", "C")]
+    n, failed = 0, []
+    for c in cases:
+        try:
+            run_case(*c)
+        except AssertionError as e:
+            failed.append(str(e))
+            print("FAIL", e, flush=True)
+        n += 1
+    dist.barrier()
+    if failed:
+        raise SystemExit(f"{len(failed)} of {n} cases failed on rank {dist.get_rank()}")
+    if dist.get_rank() == 0:
+        print(f"MP OK {n} cases on {world} ranks", flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,35 @@
+"""Multi-GPU parity through torchrun (NCCL and NVLink P2P backends).
+
+Runs tests/mp_worker.py on every visible GPU (2 or 4), one process per GPU,
+rendezvous on 127.0.0.1.  Skipped when fewer than 2 GPUs are visible.
+"""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+from tests.conftest import gpu_count
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.skipif(gpu_count() < 2, reason="needs >= 2 GPUs")
+def test_multi_gpu_parity():
+    n = 4 if gpu_count() >= 4 else 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "tests", "mp_worker.py"), os.environ.get("J3D_MP_CASES", "quick")]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert p.returncode == 0 and "MP OK" in p.stdout, p.stdout[-3000:] + p.stderr[-5000:]
