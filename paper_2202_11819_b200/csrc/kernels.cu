@@ -347,14 +347,16 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
         double* obase = d->out + (int64_t)(yl + 1) * pitch + XOFF + xl;
         const uint32_t pro = faces ? d->pro_mask : 0u;
         const uint32_t epi = faces ? d->epi_mask : 0u;
-        const bool edge_xy = x0 == 0 || x0 + T::TX + 1 >= nx || y0 == 0 || y0 + T::TY >= ny;
+        // block faces (bits 0..3 = -x,+x,-y,+y) this tile's cells touch
+        const uint32_t touch = (x0 == 0 ? 1u : 0u) | (x0 + T::TX >= nx ? 2u : 0u) | (y0 == 0 ? 4u : 0u) |
+                               (y0 + T::TY >= ny ? 8u : 0u);
         const bool whole = x0 + T::TX <= nx && y0 + T::TY <= ny;  // no cell of the tile is outside the block
         const int sbase = (warp * RPW + 1) * W + 2 * lane + 2;  // smem offset of cell (r = 0, c = 0)
 
         // wait for the stage of plane zz, patch its ghosts (fused prologue) if needed
         auto acquire = [&](int zz) {
             mbar_wait(&full[s], ph);
-            if (pro && (edge_xy || zz < 0 || zz >= nz)) {
+            if ((pro & touch) || (zz < 0 && (pro & 16u)) || (zz >= nz && (pro & 32u))) {
                 patch_stage<T>(d, stage(s), zz, x0, y0, warp, lane);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
@@ -417,7 +419,8 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                     }
                 }
             }
-            const bool face_plane = epi && (edge_xy || z == 0 || z == nz - 1);
+            const uint32_t fm = epi & (touch | (z == 0 ? 16u : 0u) | (z == nz - 1 ? 32u : 0u));
+            const bool face_plane = fm != 0;
             if (tiny || face_plane) {
 #pragma unroll
                 for (int r = 0; r < RPW; ++r) {
@@ -426,8 +429,8 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                         const int x = xl + 64 * c, y = yl + r;
                         if (y >= ny || x >= nx) continue;
                         const bool has2 = x + 1 < nx;
-                        const bool onb = face_plane && (x == 0 || x + 2 >= nx || y == 0 || y == ny - 1 || z == 0 ||
-                                                        z == nz - 1);
+                        const bool onb = ((fm & 1u) && x == 0) || ((fm & 2u) && x + 2 >= nx) ||
+                                         ((fm & 4u) && y == 0) || ((fm & 8u) && y == ny - 1) || (fm & 48u);
                         if (!tiny && !onb) continue;
                         const double* p = st + r * W + 64 * c;
                         const double2 cc = Q[r][c];
