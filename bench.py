@@ -42,6 +42,10 @@ WORKLOADS = {
     "strong3072_odf2": dict(kind="strong", global_=(3072, 3072, 3072), odf=2),
     # configs[4]: fine-grained, 768^3 global (8 GPUs x ODF 64 = 96^3 blocks)
     "fine768_odf64": dict(kind="strong", global_=(768, 768, 768), odf=64),
+    # configs[4] per GPU: 384^3 per GPU with ODF 64 = the 96^3 blocks of 768^3 on 8 GPUs
+    "fine384_odf64": dict(kind="weak", per_gpu=(384, 384, 384), odf=64),
+    # the paper's small weak-scaling problem (192^3 per node)
+    "small192_odf1": dict(kind="weak", per_gpu=(192, 192, 192), odf=1),
     # configs[0]: the small oracle-checkable case
     "small64_odf8": dict(kind="strong", global_=(64, 64, 64), odf=8),
 }

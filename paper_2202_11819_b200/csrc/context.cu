@@ -132,6 +132,8 @@ struct jacobi3d {
     WorkItem* d_items = nullptr;
     CopyDesc* d_pack = nullptr;
     CopyDesc* d_unpack = nullptr;
+    CopyDesc* d_unpack_nccl = nullptr;         // unpack of NCCL faces only (direct variant)
+    bool direct_nccl_unpack = false;
     BlockGeom* d_geom = nullptr;
     unsigned int* d_sched = nullptr;            // [2*(n_local+1)] stencil work counters
     bool store_hint = false;
@@ -343,6 +345,13 @@ void build_tables(jacobi3d* c) {
                         if (k == PEER_P2P && !c->p2p_connected) continue;  // filled after ipc_connect
                         d.epi[f] = c->layer(c->buf(c->nbr_local[l][f], q, r), f ^ 1, true);
                         d.epi_mask |= 1u << f;
+                    } else if (v == J3D_FUSE_DIRECT) {
+                        // NCCL face of the direct variant: epilogue packs into the
+                        // send buffer; after the exchange a batched unpack kernel
+                        // writes the received face into the ghost layer (keeps the
+                        // stencil's prologue empty)
+                        d.epi[f] = pack_dst(c, l, f, q);
+                        d.epi_mask |= 1u << f;
                     } else {
                         if (k == PEER_P2P && !c->p2p_connected) continue;
                         d.epi[f] = pack_dst(c, l, f, q);
@@ -379,15 +388,26 @@ void build_tables(jacobi3d* c) {
             }
     CK(cudaMemcpy(c->d_pack, pack.data(), pack.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->d_unpack, unpack.data(), unpack.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
+    // NCCL faces only (direct variant's post-exchange unpack)
+    c->direct_nccl_unpack = false;
+    for (int q = 0; q < 2; ++q)
+        for (int l = 0; l < nl; ++l)
+            for (int f = 0; f < 6; ++f) {
+                CopyDesc& up = unpack[(q * nl + l) * 6 + f];
+                if (c->kind[l][f] != PEER_NCCL) std::memset(&up, 0, sizeof up);
+                else if (v == J3D_FUSE_DIRECT) c->direct_nccl_unpack = true;
+            }
+    CK(cudaMemcpy(c->d_unpack_nccl, unpack.data(), unpack.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
 }
 
 void build_static_tables(jacobi3d* c) {
     const int nl = c->n_local;
     // ---- tensor maps [2*l + p] over each input buffer
     g_drv.load();
-    // 128x30 tiles (15 consumer warps, 4-stage ring, 1 CTA/SM) for wide
-    // blocks, 64x16 tiles (2 CTAs/SM) for narrow ones (bench sweep)
-    c->tile_kind = c->nx >= 128 ? 11 : 1;
+    // 128x30 tiles (15 consumer warps, 5-stage ring, 1 CTA/SM) for wide
+    // blocks, 64x16 tiles (3 CTAs/SM) for narrow ones; both read every value
+    // from shared memory (no register carry).  Bench sweeps: profiles/, DESIGN.md.
+    c->tile_kind = c->nx >= 128 ? 16 : 17;
     if (const char* e = std::getenv("J3D_TILE")) {  // tuning override (bench sweeps)
         const int k = std::atoi(e);
         if (k >= 0 && k < num_tile_kinds()) c->tile_kind = k;
@@ -425,7 +445,9 @@ void build_static_tables(jacobi3d* c) {
     // chunk re-reads only 2 extra planes (2% at 96).  Measured sweep: 96
     // beats 32/64/128/full depth (profiles/).
     int64_t best_zc = std::max<int64_t>(1, (c->nz + 95) / 96);
-    (void)tiles;
+    // small problems: shorter chunks until there are >= 2 items per CTA slot
+    // (at least 8 planes per chunk)
+    while (tiles * best_zc < 2 * (int64_t)c->grid_cap && c->nz / (best_zc + 1) >= 8) ++best_zc;
     if (const char* e = std::getenv("J3D_ZCHUNK")) {  // tuning override: planes per z chunk
         const int64_t L = std::atoll(e);
         if (L > 0) best_zc = std::max<int64_t>(1, (c->nz + L - 1) / L);
@@ -636,6 +658,7 @@ void enqueue_iteration(jacobi3d* c, int p, bool first, bool last) {
         if (unf) copies(c, c->d_pack, q, -1, 0, true, c->main);
         cross_gpu_exchange(c, q, q);
         if (unf) copies(c, c->d_unpack, q, -1, 0, true, c->main);
+        else if (c->direct_nccl_unpack && !c->skip_exchange) copies(c, c->d_unpack_nccl, q, -1, 0, true, c->main);
         return;
     }
     // ---- per-block streams
@@ -674,6 +697,7 @@ void enqueue_iteration(jacobi3d* c, int p, bool first, bool last) {
         for (int l = 0; l < c->n_local; ++l)
             if (c->has_peer[l]) CK(cudaStreamWaitEvent(c->main, unf ? c->ev_pk[l][q] : c->ev_st[l][q], 0));
         cross_gpu_exchange(c, q, q);
+        if (!unf && c->direct_nccl_unpack) copies(c, c->d_unpack_nccl, q, -1, 0, true, c->main);
         CK(cudaEventRecord(c->ev_xw[q], c->main));
     }
     if (unf) {
@@ -786,6 +810,7 @@ void destroy_ctx(jacobi3d* c) {
     cudaFree(c->d_items);
     cudaFree(c->d_pack);
     cudaFree(c->d_unpack);
+    cudaFree(c->d_unpack_nccl);
     cudaFree(c->d_geom);
     cudaFree(c->d_sched);
     cudaFree(c->arena);
@@ -890,6 +915,7 @@ int jacobi3d_create(const jacobi3d_config* cfg, const uint8_t* nccl_uid, jacobi3
         CK(cudaMalloc(&c->d_tmaps, sizeof(CUtensorMap) * 2 * c->n_local));
         CK(cudaMalloc(&c->d_pack, sizeof(CopyDesc) * 12 * c->n_local));
         CK(cudaMalloc(&c->d_unpack, sizeof(CopyDesc) * 12 * c->n_local));
+        CK(cudaMalloc(&c->d_unpack_nccl, sizeof(CopyDesc) * 12 * c->n_local));
         CK(cudaMalloc(&c->d_geom, sizeof(BlockGeom) * c->n_local));
         CK(cudaMalloc(&c->d_sched, sizeof(unsigned int) * 2 * (c->n_local + 1)));
         CK(cudaMemset(c->d_sched, 0, sizeof(unsigned int) * 2 * (c->n_local + 1)));

@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "device.cuh"
 #include "kernels.h"
@@ -141,9 +142,13 @@ __device__ __forceinline__ double sum7(double c, double xm, double xp, double ym
 // Tile shape: TX cells along x (a warp covers 64 with double2 per lane, CPL
 // column groups), NCW consumer warps each owning RPW rows (TY = NCW*RPW),
 // NSTAGE plane buffers in the TMA ring, MINB CTAs per SM targeted.
-template <int TX_, int NCW_, int RPW_, int NSTAGE_, int MINB_>
+template <int TX_, int NCW_, int RPW_, int NSTAGE_, int MINB_, int CARRY_ = 1>
 struct Tile {
     static constexpr int TX = TX_, NCW = NCW_, RPW = RPW_, NSTAGE = NSTAGE_, MINB = MINB_;
+    // CARRY: the centre values of planes z-1, z, z+1 live in registers (three
+    // sets in rotated roles); otherwise every value is read from shared
+    // memory and three plane stages are held (fewer registers, one code copy)
+    static constexpr bool CARRY = CARRY_ != 0;
     static constexpr int TY = NCW * RPW;
     static constexpr int CPL = TX / 64;
     static constexpr int W = TX + 4;  // smem row: x0-2 .. x0+TX+1 (16-B aligned interior)
@@ -152,7 +157,7 @@ struct Tile {
     static constexpr int STAGE_BYTES = (W * H * 8 + 127) / 128 * 128;
     static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8 + 2 * 4 * 8 + 4 * 4 + 128;
     static constexpr int THREADS = 32 * (NCW + 1);
-    static_assert(TX % 64 == 0 && W <= 256 && H <= 256 && NSTAGE >= 3, "tile shape");
+    static_assert(TX % 64 == 0 && W <= 256 && H <= 256 && NSTAGE >= (CARRY ? 3 : 4), "tile shape");
 };
 
 // Rare path (strategy C prologue, "unpack fused into the update"): overwrite
@@ -218,9 +223,8 @@ __device__ __forceinline__ void patch_stage(const StencilDesc* __restrict__ d, d
 
 // Rare path (strategy C / direct epilogue, "pack fused into the update"):
 // store the new values of a boundary cell pair to the face destinations.
-__device__ __forceinline__ void epi_store(const StencilDesc* __restrict__ d, int x, int y, int z, double vx, double vy,
-                                       bool has2) {
-    const uint32_t epi = d->epi_mask;
+__device__ __forceinline__ void epi_store(const StencilDesc* __restrict__ d, uint32_t epi, int x, int y, int z,
+                                          double vx, double vy, bool has2) {
     const int nx = d->nx, ny = d->ny, nz = d->nz;
     if ((epi & 1u) && x == 0) { const FaceRef f = load_face(&d->epi[0]); f.p[y * f.sa + z * f.sb] = vx; }
     if (epi & 2u) {
@@ -369,59 +373,106 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                 for (int c = 0; c < CPL; ++c) v[r][c] = *reinterpret_cast<const double2*>(st + sbase + r * W + 64 * c);
         };
 
-        double2 A[RPW][CPL], B[RPW][CPL], C[RPW][CPL];
-        acquire(w.z0 - 1);
-        read_centres(stage(s), A);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        advance();
-        acquire(w.z0);
-        read_centres(stage(s), B);
-        int scur = s;
-        advance();
-
-        // One output plane z from (P = z-1, Q = z, N <- z+1), called with the
-        // three register sets in rotated roles so no register moves are needed.
-        // Hot part: no branches but the store predicates.  Rare part (a tiny
-        // sum needing the subnormal-exact division, or a plane with fused-
-        // epilogue faces): recompute the cells from the same inputs and store
-        // again / store the face values.
-        auto plane = [&](int z, const double2 (&P)[RPW][CPL], const double2 (&Q)[RPW][CPL],
-                         double2 (&N)[RPW][CPL]) {
-            acquire(z + 1);
-            read_centres(stage(s), N);
-            const double* st = stage(scur) + sbase;
+        // One output plane z.  Hot part: no branches but the store
+        // predicates.  Rare part (a tiny sum needing the subnormal-exact
+        // division, or x faces of the fused epilogue): recompute those cells
+        // from the same inputs and store again / store the face values.
+        // st: stage of plane z (+ this thread's offset); CC/ZM/ZP give the
+        // centre values of planes z, z-1, z+1 for cell pair (r, c).
+        auto compute_plane_t = [&](auto faces_tag, int z, uint32_t fm, const double* st, auto&& CC, auto&& ZM,
+                                   auto&& ZP) {
+            constexpr bool FACES = decltype(faces_tag)::value;
             double* op = obase + (int64_t)(z + 1) * zs;
+            // Fused epilogue ("pack fused into the update"): faces this plane
+            // feeds are stored inline next to the output -- z faces (the whole
+            // plane) and y faces (whole rows) as 16-byte stores where aligned,
+            // x faces (one cell per row) by the owning lane.  Only the
+            // degenerate nz == 1 case (two z faces) uses the rare pass.
+            double* zdst = nullptr;
+            int64_t zsb = 0;
+            double* ymd = nullptr;
+            double* ypd = nullptr;
+            double* xmd = nullptr;
+            double* xpd = nullptr;
+            int64_t xmsa = 0, xpsa = 0;
+            uint32_t rare_faces = 0;
+            if (FACES && (fm & 1u)) {
+                const FaceRef F = load_face(&d->epi[0]);
+                xmd = F.p + (int64_t)z * F.sb;
+                xmsa = F.sa;
+            }
+            if (FACES && (fm & 2u)) {
+                const FaceRef F = load_face(&d->epi[1]);
+                xpd = F.p + (int64_t)z * F.sb;
+                xpsa = F.sa;
+            }
+            if (FACES && (fm & ~3u)) {
+                if ((fm & 48u) == 48u) {
+                    rare_faces |= 48u;
+                } else if (fm & 48u) {
+                    const FaceRef F = load_face(&d->epi[(fm & 16u) ? 4 : 5]);
+                    zdst = F.p;
+                    zsb = F.sb;
+                }
+                if (fm & 4u) {
+                    const FaceRef F = load_face(&d->epi[2]);
+                    ymd = F.p + (int64_t)z * F.sb;
+                }
+                if (fm & 8u) {
+                    const FaceRef F = load_face(&d->epi[3]);
+                    ypd = F.p + (int64_t)z * F.sb;
+                }
+            }
             bool tiny = false;
 #pragma unroll
             for (int r = 0; r < RPW; ++r) {
 #pragma unroll
                 for (int c = 0; c < CPL; ++c) {
                     const double* p = st + r * W + 64 * c;
-                    const double2 cc = Q[r][c];
+                    const double2 cc = CC(r, c);
                     const double2 ym = *reinterpret_cast<const double2*>(p - W);
                     const double2 yp = *reinterpret_cast<const double2*>(p + W);
-                    const double s0 = sum7(cc.x, p[-1], cc.y, ym.x, yp.x, P[r][c].x, N[r][c].x);
-                    const double s1 = sum7(cc.y, cc.x, p[2], ym.y, yp.y, P[r][c].y, N[r][c].y);
+                    const double s0 = sum7(cc.x, p[-1], cc.y, ym.x, yp.x, ZM(r, c).x, ZP(r, c).x);
+                    const double s1 = sum7(cc.y, cc.x, p[2], ym.y, yp.y, ZM(r, c).y, ZP(r, c).y);
                     tiny |= (fabs(s0) < kDiv7Tiny) | (fabs(s1) < kDiv7Tiny);
                     const double vx = div7_fast(s0), vy = div7_fast(s1);
                     double* o = op + r * pitch + 64 * c;
                     const int x = xl + 64 * c, y = yl + r;
-                    if (whole || (y < ny && x + 1 < nx)) {
+                    const bool v1 = whole || (y < ny && x + 1 < nx);
+                    const bool v0 = v1 || (y < ny && x < nx);
+                    if (v1) {
                         if (hint)
                             asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(o), "d"(vx),
                                          "d"(vy), "l"(store_policy)
                                          : "memory");
                         else
                             *reinterpret_cast<double2*>(o) = make_double2(vx, vy);
-                    } else if (y < ny && x < nx) {
+                    } else if (v0) {
                         o[0] = vx;
+                    }
+                    if (FACES && xmd && x == 0 && v0) xmd[y * xmsa] = vx;
+                    if (FACES && xpd && v0) {
+                        if (x == nx - 1) xpd[y * xpsa] = vx;
+                        else if (x + 1 == nx - 1) xpd[y * xpsa] = vy;
+                    }
+                    if (FACES && (fm & ~3u)) {
+                        double* fd[3] = {zdst ? zdst + x + (int64_t)y * zsb : nullptr,
+                                         (ymd && y == 0) ? ymd + x : nullptr, (ypd && y == ny - 1) ? ypd + x : nullptr};
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) {
+                            double* q = fd[k];
+                            if (!q) continue;
+                            if (v1 && !(reinterpret_cast<uintptr_t>(q) & 15)) {
+                                *reinterpret_cast<double2*>(q) = make_double2(vx, vy);
+                            } else {
+                                if (v0) q[0] = vx;
+                                if (v1) q[1] = vy;
+                            }
+                        }
                     }
                 }
             }
-            const uint32_t fm = epi & (touch | (z == 0 ? 16u : 0u) | (z == nz - 1 ? 32u : 0u));
-            const bool face_plane = fm != 0;
-            if (tiny || face_plane) {
+            if (tiny || (FACES && rare_faces)) {
 #pragma unroll
                 for (int r = 0; r < RPW; ++r) {
 #pragma unroll
@@ -429,35 +480,91 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                         const int x = xl + 64 * c, y = yl + r;
                         if (y >= ny || x >= nx) continue;
                         const bool has2 = x + 1 < nx;
-                        const bool onb = ((fm & 1u) && x == 0) || ((fm & 2u) && x + 2 >= nx) ||
-                                         ((fm & 4u) && y == 0) || ((fm & 8u) && y == ny - 1) || (fm & 48u);
+                        const bool onb = (rare_faces & 48u) != 0;
                         if (!tiny && !onb) continue;
                         const double* p = st + r * W + 64 * c;
-                        const double2 cc = Q[r][c];
+                        const double2 cc = CC(r, c);
                         const double2 ym = *reinterpret_cast<const double2*>(p - W);
                         const double2 yp = *reinterpret_cast<const double2*>(p + W);
-                        const double vx = div7(sum7(cc.x, p[-1], cc.y, ym.x, yp.x, P[r][c].x, N[r][c].x));
-                        const double vy = div7(sum7(cc.y, cc.x, p[2], ym.y, yp.y, P[r][c].y, N[r][c].y));
+                        const double vx = div7(sum7(cc.x, p[-1], cc.y, ym.x, yp.x, ZM(r, c).x, ZP(r, c).x));
+                        const double vy = div7(sum7(cc.y, cc.x, p[2], ym.y, yp.y, ZM(r, c).y, ZP(r, c).y));
                         double* o = op + r * pitch + 64 * c;
                         o[0] = vx;
                         if (has2) o[1] = vy;
-                        if (onb) epi_store(d, x, y, z, vx, vy, has2);
+                        // tiny sums: redo every face store of this cell with the exact value
+                        const uint32_t m = tiny ? fm : (rare_faces & fm);
+                        if (m) epi_store(d, m, x, y, z, vx, vy, has2);
                     }
                 }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[scur]);
-            scur = s;
-            advance();
+        };
+        // planes without face work (the vast majority) run a loop with no
+        // epilogue code at all
+        auto compute_plane = [&](int z, const double* st, auto&& CC, auto&& ZM, auto&& ZP) {
+            const uint32_t fm = epi & (touch | (z == 0 ? 16u : 0u) | (z == nz - 1 ? 32u : 0u));
+            if (fm) compute_plane_t(std::true_type{}, z, fm, st, CC, ZM, ZP);
+            else compute_plane_t(std::false_type{}, z, 0u, st, CC, ZM, ZP);
         };
 
-        for (int z = w.z0;;) {
-            if (z >= w.z1) break;
-            plane(z++, A, B, C);
-            if (z >= w.z1) break;
-            plane(z++, B, C, A);
-            if (z >= w.z1) break;
-            plane(z++, C, A, B);
+        int scur;
+        if constexpr (T::CARRY) {
+            double2 A[RPW][CPL], B[RPW][CPL], C[RPW][CPL];
+            acquire(w.z0 - 1);
+            read_centres(stage(s), A);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            advance();
+            acquire(w.z0);
+            read_centres(stage(s), B);
+            scur = s;
+            advance();
+            // (P = z-1, Q = z, N <- z+1) in rotated roles: no register moves
+            auto plane = [&](int z, const double2 (&P)[RPW][CPL], const double2 (&Q)[RPW][CPL],
+                             double2 (&N)[RPW][CPL]) {
+                acquire(z + 1);
+                read_centres(stage(s), N);
+                compute_plane(
+                    z, stage(scur) + sbase, [&](int r, int c) { return Q[r][c]; },
+                    [&](int r, int c) { return P[r][c]; }, [&](int r, int c) { return N[r][c]; });
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[scur]);
+                scur = s;
+                advance();
+            };
+            for (int z = w.z0;;) {
+                if (z >= w.z1) break;
+                plane(z++, A, B, C);
+                if (z >= w.z1) break;
+                plane(z++, B, C, A);
+                if (z >= w.z1) break;
+                plane(z++, C, A, B);
+            }
+        } else {
+            // stages of planes z-1, z, z+1 are held; everything read from smem
+            acquire(w.z0 - 1);
+            int sm = s;
+            advance();
+            acquire(w.z0);
+            scur = s;
+            advance();
+            for (int z = w.z0; z < w.z1; ++z) {
+                acquire(z + 1);
+                const int sp = s;
+                advance();
+                const double* pm = stage(sm) + sbase;
+                const double* pc = stage(scur) + sbase;
+                const double* pp = stage(sp) + sbase;
+                compute_plane(
+                    z, pc, [&](int r, int c) { return *reinterpret_cast<const double2*>(pc + r * W + 64 * c); },
+                    [&](int r, int c) { return *reinterpret_cast<const double2*>(pm + r * W + 64 * c); },
+                    [&](int r, int c) { return *reinterpret_cast<const double2*>(pp + r * W + 64 * c); });
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[sm]);
+                sm = scur;
+                scur = sp;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[sm]);  // plane z1-1
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[scur]);  // plane z1
@@ -589,20 +696,26 @@ cudaError_t launch_div7_selftest(uint64_t n, uint64_t seed, unsigned long long* 
 // ------------------------------------------------------------------ host launchers
 // Tile configurations selectable at run time (kind index):
 //          TX  NCW RPW NSTAGE MINB      tile     CTAs/SM (smem)
-#define J3D_TILES(X)                                                        \
-    X(0, 128, 8, 2, 4, 2)   /* 128x16, 4 x 19 KB stages                */ \
-    X(1, 64, 8, 2, 4, 2)    /* 64x16, 4 x 9.8 KB                       */ \
-    X(2, 64, 8, 2, 6, 2)    /* 64x16, 6 stages                         */ \
-    X(3, 128, 8, 2, 8, 1)   /* 128x16, 8 stages, 1 CTA/SM              */ \
-    X(4, 128, 8, 1, 6, 2)   /* 128x8, 6 x 10.5 KB                      */ \
-    X(5, 64, 16, 2, 6, 1)   /* 64x32, 16 consumer warps                */ \
-    X(6, 64, 16, 1, 6, 2)   /* 64x16, 16 consumer warps                */ \
-    X(7, 64, 8, 1, 6, 3)    /* 64x8, 3 CTAs/SM                         */ \
-    X(8, 64, 8, 2, 4, 3)    /* 64x16, 3 CTAs/SM                        */ \
-    X(9, 128, 16, 1, 4, 1)  /* 128x16, 16 consumer warps, 1 CTA/SM     */ \
-    X(10, 128, 8, 1, 8, 2)  /* 128x8, 8 stages                         */ \
-    X(11, 128, 15, 2, 4, 1) /* 128x30, 15 consumer warps, 4 x 34 KB    */ \
-    X(12, 128, 11, 2, 6, 1) /* 128x22, 11 consumer warps, 6 x 25 KB    */
+#define J3D_TILES(X)                                                             \
+    X(0, 128, 8, 2, 4, 2, 1)    /* 128x16, 4 x 19 KB stages                    */ \
+    X(1, 64, 8, 2, 4, 2, 1)     /* 64x16, 4 x 9.8 KB                           */ \
+    X(2, 64, 8, 2, 6, 2, 1)     /* 64x16, 6 stages                             */ \
+    X(3, 128, 8, 2, 8, 1, 1)    /* 128x16, 8 stages, 1 CTA/SM                  */ \
+    X(4, 128, 8, 1, 6, 2, 1)    /* 128x8, 6 x 10.5 KB                          */ \
+    X(5, 64, 16, 2, 6, 1, 1)    /* 64x32, 16 consumer warps                    */ \
+    X(6, 64, 16, 1, 6, 2, 1)    /* 64x16, 16 consumer warps                    */ \
+    X(7, 64, 8, 1, 6, 3, 1)     /* 64x8, 3 CTAs/SM                             */ \
+    X(8, 64, 8, 2, 4, 3, 1)     /* 64x16, 3 CTAs/SM                            */ \
+    X(9, 128, 16, 1, 4, 1, 1)   /* 128x16, 16 consumer warps, 1 CTA/SM         */ \
+    X(10, 128, 8, 1, 8, 2, 1)   /* 128x8, 8 stages                             */ \
+    X(11, 128, 15, 2, 4, 1, 1)  /* 128x30, 15 consumer warps, 4 x 34 KB        */ \
+    X(12, 128, 11, 2, 6, 1, 1)  /* 128x22, 11 consumer warps, 6 x 25 KB        */ \
+    X(13, 128, 15, 2, 6, 1, 0)  /* 128x30 from smem only, 6 x 34 KB            */ \
+    X(14, 128, 8, 2, 5, 2, 0)   /* 128x16 from smem only, 5 x 19 KB, 2 CTA/SM  */ \
+    X(15, 64, 8, 2, 6, 2, 0)    /* 64x16 from smem only                        */ \
+    X(16, 128, 15, 2, 5, 1, 0)  /* 128x30 from smem only, 5 stages             */ \
+    X(17, 64, 8, 2, 7, 3, 0)    /* 64x16 from smem only, 3 CTAs/SM             */ \
+    X(18, 128, 8, 1, 8, 2, 0)   /* 128x8 from smem only, 8 stages              */
 
 template <class T>
 static cudaError_t launch_t(const StencilLaunch& L, cudaStream_t st) {
@@ -628,13 +741,13 @@ static cudaError_t occ_t(int* blocks) {
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, stencil_tma_kernel<T>, T::THREADS, T::SMEM_BYTES);
 }
 
-#define J3D_TYPE(k, tx, ncw, rpw, ns, mb) Tile<tx, ncw, rpw, ns, mb>
+#define J3D_TYPE(k, tx, ncw, rpw, ns, mb, cy) Tile<tx, ncw, rpw, ns, mb, cy>
 
-int num_tile_kinds() { return 13; }
+int num_tile_kinds() { return 19; }
 
 TileShape tile_shape(int kind) {
     switch (kind) {
-#define X(k, tx, ncw, rpw, ns, mb) \
+#define X(k, tx, ncw, rpw, ns, mb, cy) \
     case k: return TileShape{tx, ncw * rpw};
         J3D_TILES(X)
 #undef X
@@ -644,8 +757,8 @@ TileShape tile_shape(int kind) {
 
 cudaError_t launch_stencil(const StencilLaunch& L, cudaStream_t st) {
     switch (L.kind) {
-#define X(k, tx, ncw, rpw, ns, mb) \
-    case k: return launch_t<J3D_TYPE(k, tx, ncw, rpw, ns, mb)>(L, st);
+#define X(k, tx, ncw, rpw, ns, mb, cy) \
+    case k: return launch_t<J3D_TYPE(k, tx, ncw, rpw, ns, mb, cy)>(L, st);
         J3D_TILES(X)
 #undef X
     }
@@ -654,8 +767,8 @@ cudaError_t launch_stencil(const StencilLaunch& L, cudaStream_t st) {
 
 cudaError_t stencil_occupancy(int kind, bool, int* blocks_per_sm) {
     switch (kind) {
-#define X(k, tx, ncw, rpw, ns, mb) \
-    case k: return occ_t<J3D_TYPE(k, tx, ncw, rpw, ns, mb)>(blocks_per_sm);
+#define X(k, tx, ncw, rpw, ns, mb, cy) \
+    case k: return occ_t<J3D_TYPE(k, tx, ncw, rpw, ns, mb, cy)>(blocks_per_sm);
         J3D_TILES(X)
 #undef X
     }
