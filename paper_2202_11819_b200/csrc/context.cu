@@ -298,6 +298,13 @@ void classify(jacobi3d* c) {
         if (c->has_peer[l]) c->order.push_back(l);
     for (int l = 0; l < c->n_local; ++l)
         if (!c->has_peer[l]) c->order.push_back(l);
+    if (const char* e = std::getenv("J3D_ORDER_SEED")) {  // test hook: perturbed launch order
+        uint64_t st = std::strtoull(e, nullptr, 10) * 0x9E3779B97F4A7C15ULL + 1;
+        for (int i = (int)c->order.size() - 1; i > 0; --i) {
+            st ^= st << 13; st ^= st >> 7; st ^= st << 17;
+            std::swap(c->order[i], c->order[(int)(st % (uint64_t)(i + 1))]);
+        }
+    }
 }
 
 // Source of the ghost values of face f of local block l for buffer parity par

@@ -189,3 +189,30 @@ def test_subnormal_values(scale_exp):
     U0[5:9, 5:9, 5:9] = -0.0
     for v in ("direct", "unfused", "C"):
         _case((40, 24, 16), 4, v, "batched", False, 9, boundary=0.0, field=U0)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_schedule_perturbation_does_not_change_bits(seed, monkeypatch):
+    """SPEC.md L425 analogue: a perturbed launch order of the per-block
+    streams (J3D_ORDER_SEED shuffles the block order) changes timings, never
+    the bits."""
+    monkeypatch.setenv("J3D_ORDER_SEED", str(seed))
+    for v in ("unfused", "A", "C", "direct"):
+        _case((48, 48, 48), 27, v, "per_block", False, 9, kind="hash", seed=seed)
+
+
+def test_medium_grid_checksums_and_determinism():
+    """T7: 256x192x160, ODF 8, 30 iterations: every variant / launch / graph
+    combination reproduces the oracle's checksum; three repeated runs of the
+    same context give identical checksums (S:571 analogue)."""
+    grid = (256, 192, 160)
+    U0 = oracle_initial(grid, "hash", seed=20220223)
+    want = core.checksum(core.run(U0, 30))
+    for v, l, g in itertools.product(VARIANTS, LAUNCHES, [False, True]):
+        with j3d.Jacobi3D(grid, odf=8, variant=v, launch=l, graph=g) as ctx:
+            sums = []
+            for _ in range(3):
+                ctx.init("hash", seed=20220223)
+                ctx.iterate(30)
+                sums.append(ctx.checksum())
+            assert sums == [want] * 3, (v, l, g)
