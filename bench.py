@@ -171,6 +171,7 @@ def parse():
     ap.add_argument("--launch", default="batched")
     ap.add_argument("--graph", type=int, default=0)
     ap.add_argument("--exchange", default="auto")
+    ap.add_argument("--overlap", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--grid", default=None, help="override global grid gx,gy,gz")
@@ -195,7 +196,7 @@ def main():
         grid = tuple(int(x) for x in a.grid.split(","))
     odf = a.odf or wl["odf"]
     cfg_json = {"workload": a.workload, "grid": list(grid), "odf": odf, "variant": a.variant, "launch": a.launch,
-                "graph": bool(a.graph), "exchange": a.exchange, "n_gpus": n,
+                "graph": bool(a.graph), "exchange": a.exchange, "overlap": bool(a.overlap), "n_gpus": n,
                 "l2": "inputs larger than L2 (no flush needed)" if grid[0] * grid[1] * grid[2] * 16 / n > 2e9
                 else "inputs smaller than L2",
                 "init": f"hash-random [0,1), seed {SEED}, Dirichlet 1.0"}
@@ -216,7 +217,7 @@ def main():
 
     if world > 1:
         ctx = jdist.create(grid, odf=odf, variant=a.variant, launch=a.launch, graph=bool(a.graph),
-                           exchange=a.exchange)
+                           exchange=a.exchange, overlap=bool(a.overlap))
     else:
         ctx = j3d.Jacobi3D(grid, odf=odf, variant=a.variant, launch=a.launch, graph=bool(a.graph),
                            exchange=a.exchange, device=local)

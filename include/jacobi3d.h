@@ -102,6 +102,12 @@ typedef struct {
     int32_t use_graph;    /* 1: capture one iteration per buffer parity into two CUDA graphs and
                              alternate them; 0: direct launches             */
     int32_t exchange;     /* J3D_XCHG_*                                                          */
+    int32_t overlap;      /* 1 (BATCHED, n_gpus > 1): update the blocks' exterior (every tile x z
+                             chunk touching a peer face) first, then run the exchange of those
+                             faces on a separate stream while the interior updates (PAPER.md
+                             Fig 1 manual overlap L79-107, overdecomposition overlap L146-156);
+                             0: update everything, then exchange                               */
+    int32_t reserved;     /* must be 0                                                           */
     double  boundary;     /* Dirichlet ghost value for DEFAULT and HASH inits (default 1.0)      */
 } jacobi3d_config;
 

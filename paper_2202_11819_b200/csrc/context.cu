@@ -133,11 +133,20 @@ struct jacobi3d {
     CopyDesc* d_pack = nullptr;
     CopyDesc* d_unpack = nullptr;
     CopyDesc* d_unpack_nccl = nullptr;         // unpack of NCCL faces only (direct variant)
+    CopyDesc* d_pack_peer = nullptr;           // peer faces only (overlap mode)
+    CopyDesc* d_unpack_peer = nullptr;
+    CopyDesc* d_pack_local = nullptr;          // same-GPU faces only (overlap mode)
+    CopyDesc* d_unpack_local = nullptr;
+    bool overlap = false;                      // exterior-first split with the exchange on `comm`
+    int n_ext = 0;                             // items [0, n_ext) touch a peer face
+    cudaStream_t xstream = nullptr;            // exchange stream (overlap mode)
+    std::array<cudaEvent_t, 2> ev_ext{}, ev_comm{};
     bool direct_nccl_unpack = false;
     BlockGeom* d_geom = nullptr;
     unsigned int* d_sched = nullptr;            // [2*(n_local+1)] stencil work counters
     bool store_hint = false;
     std::vector<int> item_begin, item_count;  // per local block, in d_items
+    std::vector<int64_t> item_cells;          // prefix sums of owned cells per item (profiling bytes)
     int n_items = 0, tile_kind = 0, grid_cap = 0;
     bool faces_fused = false;                   // stencil launches carry prologue/epilogue faces
     std::vector<int> order;                     // local blocks, peer-face blocks first
@@ -237,6 +246,7 @@ int validate_cfg(const jacobi3d_config* c) {
     if (c->exchange < J3D_XCHG_AUTO || c->exchange > J3D_XCHG_P2P) return fail(J3D_EINVAL, "unknown exchange backend");
     if (c->n_gpus < 1 || c->rank < 0 || c->rank >= c->n_gpus) return fail(J3D_EINVAL, "rank / n_gpus out of range");
     if (c->odf < 1) return fail(J3D_EINVAL, "odf must be >= 1");
+    if (c->reserved != 0 || (c->overlap != 0 && c->overlap != 1)) return fail(J3D_EINVAL, "bad overlap/reserved");
     return J3D_OK;
 }
 
@@ -405,6 +415,36 @@ void build_tables(jacobi3d* c) {
                 else if (v == J3D_FUSE_DIRECT) c->direct_nccl_unpack = true;
             }
     CK(cudaMemcpy(c->d_unpack_nccl, unpack.data(), unpack.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
+    // peer-only / local-only tables for the overlap mode
+    {
+        std::vector<CopyDesc> pk_peer(pack), up_peer(2 * nl * 6), pk_loc(pack), up_loc(2 * nl * 6);
+        std::vector<CopyDesc> up_all(2 * nl * 6);
+        for (int q = 0; q < 2; ++q)
+            for (int l = 0; l < nl; ++l)
+                for (int f = 0; f < 6; ++f) {
+                    const int i = (q * nl + l) * 6 + f;
+                    const int k = c->kind[l][f];
+                    CopyDesc up;
+                    std::memset(&up, 0, sizeof up);
+                    if (k != DIRICHLET && !(k == PEER_P2P && !c->p2p_connected)) {
+                        up.src = recv_src(c, l, f, q);
+                        up.dst = c->layer(c->buf(l, q), f, true);
+                        up.na = (int32_t)c->face_na(f);
+                        up.nb = (int32_t)c->face_nb(f);
+                    }
+                    const bool peer = k == PEER_NCCL || k == PEER_P2P;
+                    if (!peer) std::memset(&pk_peer[i], 0, sizeof(CopyDesc));
+                    if (peer || k == DIRICHLET) std::memset(&pk_loc[i], 0, sizeof(CopyDesc));
+                    if (peer) up_peer[i] = up;
+                    else if (k == LOCAL) up_loc[i] = up;
+                    if (!peer && k != LOCAL) std::memset(&up_peer[i], 0, sizeof(CopyDesc));
+                }
+        for (auto& d : up_peer) if (d.na == 0) std::memset(&d, 0, sizeof d);
+        CK(cudaMemcpy(c->d_pack_peer, pk_peer.data(), pk_peer.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->d_unpack_peer, up_peer.data(), up_peer.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->d_pack_local, pk_loc.data(), pk_loc.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->d_unpack_local, up_loc.data(), up_loc.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
+    }
 }
 
 void build_static_tables(jacobi3d* c) {
@@ -462,6 +502,13 @@ void build_static_tables(jacobi3d* c) {
     std::vector<WorkItem> items;
     c->item_begin.assign(nl, 0);
     c->item_count.assign(nl, 0);
+    auto is_peer = [&](int l, int f) { return c->kind[l][f] == PEER_NCCL || c->kind[l][f] == PEER_P2P; };
+    auto exterior = [&](const WorkItem& w) {  // does the item compute a cell adjacent to a peer face?
+        const int l = w.blk;
+        return (is_peer(l, 0) && w.tx == 0) || (is_peer(l, 1) && w.tx == ntx - 1) ||
+               (is_peer(l, 2) && w.ty == 0) || (is_peer(l, 3) && w.ty == nty - 1) ||
+               (is_peer(l, 4) && w.z0 == 0) || (is_peer(l, 5) && w.z1 == c->nz);
+    };
     for (int l : c->order) {
         c->item_begin[l] = (int)items.size();
         for (int64_t zc = 0; zc < best_zc; ++zc) {
@@ -472,7 +519,19 @@ void build_static_tables(jacobi3d* c) {
         }
         c->item_count[l] = (int)items.size() - c->item_begin[l];
     }
+    c->n_ext = 0;
+    if (c->overlap) {  // BATCHED only: exterior items of every block first (stable order otherwise)
+        std::stable_partition(items.begin(), items.end(), exterior);
+        c->n_ext = (int)std::count_if(items.begin(), items.end(), exterior);
+    }
     c->n_items = (int)items.size();
+    c->item_cells.assign(items.size() + 1, 0);
+    for (size_t i = 0; i < items.size(); ++i) {
+        const WorkItem& w = items[i];
+        const int64_t ex = std::min<int64_t>(ts.tx, c->nx - (int64_t)w.tx * ts.tx);
+        const int64_t ey = std::min<int64_t>(ts.ty, c->ny - (int64_t)w.ty * ts.ty);
+        c->item_cells[i + 1] = c->item_cells[i] + ex * ey * (w.z1 - w.z0);
+    }
     CK(cudaMalloc(&c->d_items, std::max<size_t>(1, items.size()) * sizeof(WorkItem)));
     CK(cudaMemcpy(c->d_items, items.data(), items.size() * sizeof(WorkItem), cudaMemcpyHostToDevice));
 
@@ -541,9 +600,7 @@ void stencil(jacobi3d* c, int begin, int count, int parity, cudaStream_t st, int
     if (prof) {
         CK(cudaEventRecord(e1, st));
         c->prof_events.push_back({e0, e1});
-        int64_t cells = 0;
-        if (l >= 0) cells = c->nx * c->ny * c->nz;
-        else cells = c->nx * c->ny * c->nz * c->n_local;
+        const int64_t cells = c->item_cells[begin + count] - c->item_cells[begin];  // exact owned cells updated
         c->prof_pending_bytes += 16.0 * (double)cells;
     }
 }
@@ -575,7 +632,7 @@ void copies(jacobi3d* c, CopyDesc* table, int parity, int l, int face, bool fuse
 // NCCL faces: one group per exchange on the main stream (C4).  Messages to a
 // peer are posted in the canonical order (sender block id, sender face) on
 // both sides so the k-th send matches the k-th receive.
-void nccl_exchange(jacobi3d* c, int par) {
+void nccl_exchange(jacobi3d* c, int par, cudaStream_t st) {
     struct Msg { int64_t key; int l, f; bool send; };
     std::vector<Msg> msgs;
     for (int l = 0; l < c->n_local; ++l)
@@ -591,8 +648,8 @@ void nccl_exchange(jacobi3d* c, int par) {
     for (const Msg& m : msgs) {
         const int peer = c->plan.blocks[c->plan.blocks[c->gid[m.l]].nbr[m.f]].owner;
         const size_t n = (size_t)face_cells(c->plan.ext, m.f);
-        if (m.send) NK(ncclSend(c->face_buf(m.l, m.f, par, false), n, ncclFloat64, peer, c->comm, c->main));
-        else NK(ncclRecv(c->face_buf(m.l, m.f, par, true), n, ncclFloat64, peer, c->comm, c->main));
+        if (m.send) NK(ncclSend(c->face_buf(m.l, m.f, par, false), n, ncclFloat64, peer, c->comm, st));
+        else NK(ncclRecv(c->face_buf(m.l, m.f, par, true), n, ncclFloat64, peer, c->comm, st));
     }
     NK(ncclGroupEnd());
 }
@@ -602,24 +659,24 @@ void nccl_exchange(jacobi3d* c, int par) {
 // neighbour rank's flag[s][me] (stream write = release fence after all prior
 // work on the stream, i.e. after our NVLink stores).  Wait: until own
 // flag[s][r] == 1 for every neighbour r, then reset it to 0.
-void p2p_sync(jacobi3d* c, int slot) {
+void p2p_sync(jacobi3d* c, int slot, cudaStream_t st) {
     if (!c->p2p_needed) return;
     const int n = c->n_gpus;
     for (int r : c->peer_ranks) {
         uint64_t* f = c->flags(r) + slot * n + c->rank;
-        DK(g_drv.write64((CUstream)c->main, (CUdeviceptr)f, 1, 0));
+        DK(g_drv.write64((CUstream)st, (CUdeviceptr)f, 1, 0));
     }
     for (int r : c->peer_ranks) {
         uint64_t* f = c->flags() + slot * n + r;
-        DK(g_drv.wait64((CUstream)c->main, (CUdeviceptr)f, 1, CU_STREAM_WAIT_VALUE_EQ));
-        DK(g_drv.write64((CUstream)c->main, (CUdeviceptr)f, 0, 0));
+        DK(g_drv.wait64((CUstream)st, (CUdeviceptr)f, 1, CU_STREAM_WAIT_VALUE_EQ));
+        DK(g_drv.write64((CUstream)st, (CUdeviceptr)f, 0, 0));
     }
 }
 
-void cross_gpu_exchange(jacobi3d* c, int par, int slot) {
+void cross_gpu_exchange(jacobi3d* c, int par, int slot, cudaStream_t st) {
     if (c->n_gpus == 1 || c->skip_exchange) return;
-    nccl_exchange(c, par);
-    p2p_sync(c, slot);
+    nccl_exchange(c, par, st);
+    p2p_sync(c, slot, st);
 }
 
 // Full halo refresh of buffer parity `par`: pack, exchange, unpack, batched on
@@ -630,11 +687,11 @@ void cross_gpu_exchange(jacobi3d* c, int par, int slot) {
 void refresh(jacobi3d* c, int par) {
     const int rc = (int)(c->refresh_count & 1);
     c->refresh_count++;
-    if (c->n_gpus > 1) p2p_sync(c, 4 + rc);
+    if (c->n_gpus > 1) p2p_sync(c, 4 + rc, c->main);
     copies(c, c->d_pack, par, -1, 0, true, c->main);
     if (c->n_gpus > 1) {
-        nccl_exchange(c, par);
-        p2p_sync(c, 2 + rc);
+        nccl_exchange(c, par, c->main);
+        p2p_sync(c, 2 + rc, c->main);
     }
     copies(c, c->d_unpack, par, -1, 0, true, c->main);
 }
@@ -661,9 +718,29 @@ void enqueue_iteration(jacobi3d* c, int p, bool first, bool last) {
     const int v = c->cfg.variant;
     const bool unf = unfused_family(c);
     if (c->cfg.launch == J3D_BATCHED) {
+        if (c->overlap && !c->skip_exchange) {
+            // exterior items (those touching a peer face) first; the exchange
+            // of their faces runs on `comm` while the interior items update
+            // (Fig 1 manual overlap, L79-107; ODF-driven overlap, L146-156)
+            stencil(c, 0, c->n_ext, p, c->main, -1);
+            CK(cudaEventRecord(c->ev_ext[q], c->main));
+            CK(cudaStreamWaitEvent(c->xstream, c->ev_ext[q], 0));
+            if (unf) copies(c, c->d_pack_peer, q, -1, 0, true, c->xstream);
+            cross_gpu_exchange(c, q, q, c->xstream);
+            if (unf) copies(c, c->d_unpack_peer, q, -1, 0, true, c->xstream);
+            else if (c->direct_nccl_unpack) copies(c, c->d_unpack_nccl, q, -1, 0, true, c->xstream);
+            CK(cudaEventRecord(c->ev_comm[q], c->xstream));
+            stencil(c, c->n_ext, c->n_items - c->n_ext, p, c->main, -1);
+            if (unf) {
+                copies(c, c->d_pack_local, q, -1, 0, true, c->main);
+                copies(c, c->d_unpack_local, q, -1, 0, true, c->main);
+            }
+            CK(cudaStreamWaitEvent(c->main, c->ev_comm[q], 0));
+            return;
+        }
         stencil(c, 0, c->n_items, p, c->main, -1);
         if (unf) copies(c, c->d_pack, q, -1, 0, true, c->main);
-        cross_gpu_exchange(c, q, q);
+        cross_gpu_exchange(c, q, q, c->main);
         if (unf) copies(c, c->d_unpack, q, -1, 0, true, c->main);
         else if (c->direct_nccl_unpack && !c->skip_exchange) copies(c, c->d_unpack_nccl, q, -1, 0, true, c->main);
         return;
@@ -703,7 +780,7 @@ void enqueue_iteration(jacobi3d* c, int p, bool first, bool last) {
     if (peers) {
         for (int l = 0; l < c->n_local; ++l)
             if (c->has_peer[l]) CK(cudaStreamWaitEvent(c->main, unf ? c->ev_pk[l][q] : c->ev_st[l][q], 0));
-        cross_gpu_exchange(c, q, q);
+        cross_gpu_exchange(c, q, q, c->main);
         if (!unf && c->direct_nccl_unpack) copies(c, c->d_unpack_nccl, q, -1, 0, true, c->main);
         CK(cudaEventRecord(c->ev_xw[q], c->main));
     }
@@ -803,6 +880,9 @@ void destroy_ctx(jacobi3d* c) {
     for (auto& a : c->ev_pk) for (auto e : a) if (e) cudaEventDestroy(e);
     for (auto& a : c->ev_up) for (auto e : a) if (e) cudaEventDestroy(e);
     for (auto e : c->ev_xw) if (e) cudaEventDestroy(e);
+    for (auto e : c->ev_ext) if (e) cudaEventDestroy(e);
+    for (auto e : c->ev_comm) if (e) cudaEventDestroy(e);
+    if (c->xstream) cudaStreamDestroy(c->xstream);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_t0) cudaEventDestroy(c->ev_t0);
     if (c->ev_t1) cudaEventDestroy(c->ev_t1);
@@ -818,6 +898,10 @@ void destroy_ctx(jacobi3d* c) {
     cudaFree(c->d_pack);
     cudaFree(c->d_unpack);
     cudaFree(c->d_unpack_nccl);
+    cudaFree(c->d_pack_peer);
+    cudaFree(c->d_unpack_peer);
+    cudaFree(c->d_pack_local);
+    cudaFree(c->d_unpack_local);
     cudaFree(c->d_geom);
     cudaFree(c->d_sched);
     cudaFree(c->arena);
@@ -913,6 +997,8 @@ int jacobi3d_create(const jacobi3d_config* cfg, const uint8_t* nccl_uid, jacobi3
         c->sms = prop.multiProcessorCount;
         classify(c);
         build_layout(c);
+        c->overlap = cfg->overlap && cfg->launch == J3D_BATCHED && c->n_gpus > 1 &&
+                     std::any_of(c->has_peer.begin(), c->has_peer.end(), [](uint8_t h) { return h != 0; });
         CK(cudaMalloc(&c->arena, (size_t)c->arena_bytes));
         CK(cudaMemset(c->arena, 0, 4096));
         // face buffers start zeroed; done here, before any peer can map the
@@ -923,6 +1009,10 @@ int jacobi3d_create(const jacobi3d_config* cfg, const uint8_t* nccl_uid, jacobi3
         CK(cudaMalloc(&c->d_pack, sizeof(CopyDesc) * 12 * c->n_local));
         CK(cudaMalloc(&c->d_unpack, sizeof(CopyDesc) * 12 * c->n_local));
         CK(cudaMalloc(&c->d_unpack_nccl, sizeof(CopyDesc) * 12 * c->n_local));
+        CK(cudaMalloc(&c->d_pack_peer, sizeof(CopyDesc) * 12 * c->n_local));
+        CK(cudaMalloc(&c->d_unpack_peer, sizeof(CopyDesc) * 12 * c->n_local));
+        CK(cudaMalloc(&c->d_pack_local, sizeof(CopyDesc) * 12 * c->n_local));
+        CK(cudaMalloc(&c->d_unpack_local, sizeof(CopyDesc) * 12 * c->n_local));
         CK(cudaMalloc(&c->d_geom, sizeof(BlockGeom) * c->n_local));
         CK(cudaMalloc(&c->d_sched, sizeof(unsigned int) * 2 * (c->n_local + 1)));
         CK(cudaMemset(c->d_sched, 0, sizeof(unsigned int) * 2 * (c->n_local + 1)));
@@ -954,6 +1044,11 @@ int jacobi3d_create(const jacobi3d_config* cfg, const uint8_t* nccl_uid, jacobi3
             }
         mk(&c->ev_xw[0]);
         mk(&c->ev_xw[1]);
+        for (int p = 0; p < 2; ++p) {
+            mk(&c->ev_ext[p]);
+            mk(&c->ev_comm[p]);
+        }
+        if (c->overlap) CK(cudaStreamCreateWithPriority(&c->xstream, cudaStreamNonBlocking, hi_pr));
         mk(&c->ev_fork);
         CK(cudaEventCreate(&c->ev_t0));
         CK(cudaEventCreate(&c->ev_t1));

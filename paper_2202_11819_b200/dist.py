@@ -34,7 +34,7 @@ def bootstrap_bytes(make_uid, record: bytes | None = None, group=None):
 
 
 def create(grid, odf=1, variant="direct", launch="batched", graph=False, exchange="auto", boundary=1.0,
-           block=(0, 0, 0), device=None):
+           block=(0, 0, 0), device=None, overlap=False):
     """Collective: build one Jacobi3D context per rank and connect P2P peers."""
     from .jacobi3d import Jacobi3D, nccl_unique_id
 
@@ -44,7 +44,7 @@ def create(grid, odf=1, variant="direct", launch="batched", graph=False, exchang
     if world > 1:
         uid, _ = bootstrap_bytes(nccl_unique_id)
     ctx = Jacobi3D(grid, odf=odf, n_gpus=world, rank=rank, device=local, block=block, variant=variant,
-                   launch=launch, graph=graph, exchange=exchange, boundary=boundary, nccl_uid=uid)
+                   launch=launch, graph=graph, exchange=exchange, boundary=boundary, nccl_uid=uid, overlap=overlap)
     if world > 1:
         _, recs = bootstrap_bytes(lambda: None, ctx.ipc_export())
         ctx.ipc_connect(recs)

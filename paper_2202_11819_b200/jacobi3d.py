@@ -32,7 +32,8 @@ class Config(ctypes.Structure):
                 ("bx", ctypes.c_int64), ("by", ctypes.c_int64), ("bz", ctypes.c_int64),
                 ("odf", ctypes.c_int32), ("n_gpus", ctypes.c_int32), ("rank", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("variant", ctypes.c_int32), ("launch", ctypes.c_int32),
-                ("use_graph", ctypes.c_int32), ("exchange", ctypes.c_int32), ("boundary", ctypes.c_double)]
+                ("use_graph", ctypes.c_int32), ("exchange", ctypes.c_int32), ("overlap", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("boundary", ctypes.c_double)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -106,11 +107,12 @@ def _enum(table, v):
 
 
 def make_config(grid, odf=1, n_gpus=1, rank=0, device=0, block=(0, 0, 0), variant="direct", launch="batched",
-                graph=False, exchange="auto", boundary=1.0) -> Config:
+                graph=False, exchange="auto", boundary=1.0, overlap=False) -> Config:
     gx, gy, gz = grid
     bx, by, bz = block
     return Config(gx, gy, gz, bx, by, bz, odf, n_gpus, rank, device, _enum(VARIANTS, variant),
-                  _enum(LAUNCHES, launch), int(bool(graph)), _enum(EXCHANGES, exchange), boundary)
+                  _enum(LAUNCHES, launch), int(bool(graph)), _enum(EXCHANGES, exchange), int(bool(overlap)), 0,
+                  boundary)
 
 
 def plan(grid, odf=1, n_gpus=1, block=(0, 0, 0), rank=0) -> dict:
@@ -141,8 +143,10 @@ class Jacobi3D:
     """One rank's Jacobi3D context (jacobi3d_create ... jacobi3d_destroy)."""
 
     def __init__(self, grid, odf=1, n_gpus=1, rank=0, device=0, block=(0, 0, 0), variant="direct",
-                 launch="batched", graph=False, exchange="auto", boundary=1.0, nccl_uid: bytes | None = None):
-        self.cfg = make_config(grid, odf, n_gpus, rank, device, block, variant, launch, graph, exchange, boundary)
+                 launch="batched", graph=False, exchange="auto", boundary=1.0, nccl_uid: bytes | None = None,
+                 overlap=False):
+        self.cfg = make_config(grid, odf, n_gpus, rank, device, block, variant, launch, graph, exchange, boundary,
+                               overlap)
         self._h = ctypes.c_void_p()
         uid = None
         if nccl_uid is not None:

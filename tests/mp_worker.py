@@ -20,8 +20,9 @@ from oracle import core  # noqa: E402
 from paper_2202_11819_b200 import dist as jdist  # noqa: E402
 
 
-def run_case(grid, odf, variant, launch, graph, exchange, n, kind, seed):
-    ctx = jdist.create(grid, odf=odf, variant=variant, launch=launch, graph=graph, exchange=exchange)
+def run_case(grid, odf, variant, launch, graph, exchange, n, kind, seed, overlap=False):
+    ctx = jdist.create(grid, odf=odf, variant=variant, launch=launch, graph=graph, exchange=exchange,
+                       overlap=overlap)
     try:
         ctx.init(kind, seed=seed)
         ctx.iterate(n)
@@ -67,6 +68,15 @@ def main():
         cases.append((g, 4, variant, launch, graph, exchange, 9, "hash", 3))
     cases.append((g, 1, "direct", "batched", False, "p2p", 12, "default", 0))
     cases.append((g, 1, "unfused", "batched", False, "nccl", 12, "default", 0))
+    # x split across GPUs (peer x faces: strided NVLink stores / strided NCCL faces)
+    gx = (96, 48, 48) if world >= 4 else (96, 40, 40)
+    for exchange, variant in itertools.product(["p2p", "nccl"], ["direct", "C", "unfused"]):
+        cases.append((gx, 2, variant, "batched", False, exchange, 6, "hash", 5))
+    # exterior-first overlap (BATCHED), with and without graphs, every variant and backend
+    for exchange, variant, graph in itertools.product(["p2p", "nccl"], ["direct", "C", "unfused", "A"],
+                                                      [False, True]):
+        cases.append((g, 4, variant, "batched", graph, exchange, 7, "hash", 2, True))
+        cases.append((g, 1, variant, "batched", graph, exchange, 5, "hash", 2, True))
     cases.append(((45, 34, 44), 2, "direct", "batched", False, "p2p", 7, "hash", 1))
     cases.append(((45, 34, 44), 2, "C", "per_block", False, "nccl", 7, "hash", 1))
     if which == "debug":
