@@ -79,6 +79,9 @@ extern "C" {
 #define J3D_XCHG_AUTO    0  /* P2P when every peer is reachable over NVLink, else NCCL          */
 #define J3D_XCHG_NCCL    1  /* grouped ncclSend/ncclRecv, one group per iteration               */
 #define J3D_XCHG_P2P     2  /* direct NVLink stores into the peer's buffers + epoch flags       */
+#define J3D_XCHG_HOST    3  /* host staging (the paper's Charm-H / MPI-H):
+                               device send buffer -> D2H into pinned POSIX shared memory ->
+                               the neighbour's H2D into its receive buffer; same-node ranks   */
 
 /* ---- initial conditions (readings R6, R7, R12) ---------------- */
 #define J3D_INIT_DEFAULT 0  /* owned 0.0, global ghost shell = boundary             */

@@ -22,6 +22,10 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <array>
 #include <cstdio>
@@ -91,7 +95,10 @@ struct Driver {
 };
 static Driver g_drv;
 
-enum FaceKind { DIRICHLET = 0, LOCAL = 1, PEER_NCCL = 2, PEER_P2P = 3 };
+enum FaceKind { DIRICHLET = 0, LOCAL = 1, PEER_NCCL = 2, PEER_P2P = 3, PEER_HOST = 4 };
+// faces whose data travels through the send/receive buffers in a separate exchange step
+static inline bool via_buffers(int k) { return k == PEER_NCCL || k == PEER_HOST; }
+static inline bool is_peer_kind(int k) { return k == PEER_NCCL || k == PEER_P2P || k == PEER_HOST; }
 
 static inline int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
@@ -125,6 +132,14 @@ struct jacobi3d {
     int64_t faces_per_block_bytes = 0;
     std::vector<char*> peer_base;  // mapped arenas (index = rank), nullptr for self
     bool p2p_needed = false, p2p_connected = false;
+    // host staging (J3D_XCHG_HOST): one POSIX shared-memory segment per rank,
+    // [flags: 8 slots x n_gpus uint64 | staging: per local block, face, parity],
+    // registered with CUDA so stream memory ops and DMA copies reach it
+    bool host_needed = false, host_connected = false;
+    uint64_t job_key = 0;
+    size_t shm_bytes = 0;
+    std::vector<char*> shm_base;      // mapped segments (index = rank; own included)
+    std::vector<char*> shm_dev;       // device-visible address of each mapped segment
 
     // device tables
     StencilDesc* d_descs = nullptr;
@@ -243,7 +258,7 @@ int validate_cfg(const jacobi3d_config* c) {
     if (!c) return fail(J3D_EINVAL, "config is NULL");
     if (c->variant < J3D_UNFUSED || c->variant > J3D_FUSE_DIRECT) return fail(J3D_EINVAL, "unknown variant");
     if (c->launch != J3D_PER_BLOCK && c->launch != J3D_BATCHED) return fail(J3D_EINVAL, "unknown launch mode");
-    if (c->exchange < J3D_XCHG_AUTO || c->exchange > J3D_XCHG_P2P) return fail(J3D_EINVAL, "unknown exchange backend");
+    if (c->exchange < J3D_XCHG_AUTO || c->exchange > J3D_XCHG_HOST) return fail(J3D_EINVAL, "unknown exchange backend");
     if (c->n_gpus < 1 || c->rank < 0 || c->rank >= c->n_gpus) return fail(J3D_EINVAL, "rank / n_gpus out of range");
     if (c->odf < 1) return fail(J3D_EINVAL, "odf must be >= 1");
     if (c->reserved != 0 || (c->overlap != 0 && c->overlap != 1)) return fail(J3D_EINVAL, "bad overlap/reserved");
@@ -293,7 +308,8 @@ void classify(jacobi3d* c) {
                 if (n.owner == c->rank) {
                     c->kind[l][f] = LOCAL;
                 } else {
-                    c->kind[l][f] = xchg == J3D_XCHG_NCCL ? PEER_NCCL : PEER_P2P;
+                    c->kind[l][f] = xchg == J3D_XCHG_NCCL ? PEER_NCCL : xchg == J3D_XCHG_HOST ? PEER_HOST : PEER_P2P;
+                    if (xchg == J3D_XCHG_HOST) c->host_needed = true;
                     c->has_peer[l] = 1;
                     if (std::find(peers.begin(), peers.end(), n.owner) == peers.end()) peers.push_back(n.owner);
                     if (xchg == J3D_XCHG_P2P) c->p2p_needed = true;
@@ -411,7 +427,7 @@ void build_tables(jacobi3d* c) {
         for (int l = 0; l < nl; ++l)
             for (int f = 0; f < 6; ++f) {
                 CopyDesc& up = unpack[(q * nl + l) * 6 + f];
-                if (c->kind[l][f] != PEER_NCCL) std::memset(&up, 0, sizeof up);
+                if (!via_buffers(c->kind[l][f])) std::memset(&up, 0, sizeof up);
                 else if (v == J3D_FUSE_DIRECT) c->direct_nccl_unpack = true;
             }
     CK(cudaMemcpy(c->d_unpack_nccl, unpack.data(), unpack.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
@@ -432,7 +448,7 @@ void build_tables(jacobi3d* c) {
                         up.na = (int32_t)c->face_na(f);
                         up.nb = (int32_t)c->face_nb(f);
                     }
-                    const bool peer = k == PEER_NCCL || k == PEER_P2P;
+                    const bool peer = is_peer_kind(k);
                     if (!peer) std::memset(&pk_peer[i], 0, sizeof(CopyDesc));
                     if (peer || k == DIRICHLET) std::memset(&pk_loc[i], 0, sizeof(CopyDesc));
                     if (peer) up_peer[i] = up;
@@ -502,7 +518,7 @@ void build_static_tables(jacobi3d* c) {
     std::vector<WorkItem> items;
     c->item_begin.assign(nl, 0);
     c->item_count.assign(nl, 0);
-    auto is_peer = [&](int l, int f) { return c->kind[l][f] == PEER_NCCL || c->kind[l][f] == PEER_P2P; };
+    auto is_peer = [&](int l, int f) { return is_peer_kind(c->kind[l][f]); };
     auto exterior = [&](const WorkItem& w) {  // does the item compute a cell adjacent to a peer face?
         const int l = w.blk;
         return (is_peer(l, 0) && w.tx == 0) || (is_peer(l, 1) && w.tx == ntx - 1) ||
@@ -673,10 +689,123 @@ void p2p_sync(jacobi3d* c, int slot, cudaStream_t st) {
     }
 }
 
+// ---------------------------------------------------------------- host staging
+int64_t shm_flags_bytes(const jacobi3d* c) { return align_up(8 * 8 * (int64_t)c->n_gpus, 4096); }
+int64_t shm_area_offset(const jacobi3d* c, int l, int f, int par) {
+    int64_t o = shm_flags_bytes(c) + (int64_t)l * 2 * [&] {
+        int64_t t = 0;
+        for (int g = 0; g < 6; ++g) t += c->face_bytes[g];
+        return t;
+    }();
+    for (int g = 0; g < f; ++g) o += 2 * c->face_bytes[g];
+    return o + par * c->face_bytes[f];
+}
+std::string shm_name(uint64_t key, int rank) {
+    char b[64];
+    std::snprintf(b, sizeof b, "/j3d_%016llx_%d", (unsigned long long)key, rank);
+    return b;
+}
+
+void host_setup_own(jacobi3d* c) {  // at create: own segment (peers map it in ipc_connect)
+    int64_t per_block = 0;
+    for (int g = 0; g < 6; ++g) per_block += 2 * c->face_bytes[g];
+    c->shm_bytes = (size_t)(shm_flags_bytes(c) + per_block * c->n_local);
+    c->shm_base.assign(c->n_gpus, nullptr);
+    c->shm_dev.assign(c->n_gpus, nullptr);
+    const std::string nm = shm_name(c->job_key, c->rank);
+    shm_unlink(nm.c_str());
+    const int fd = shm_open(nm.c_str(), O_CREAT | O_RDWR, 0600);
+    if (fd < 0) throw Error(J3D_ENOMEM, "shm_open " + nm + " failed");
+    if (ftruncate(fd, (off_t)c->shm_bytes) != 0) {
+        close(fd);
+        throw Error(J3D_ENOMEM, "ftruncate of the staging segment failed");
+    }
+    void* p = mmap(nullptr, c->shm_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) throw Error(J3D_ENOMEM, "mmap of the staging segment failed");
+    std::memset(p, 0, (size_t)shm_flags_bytes(c));
+    c->shm_base[c->rank] = (char*)p;
+    CK(cudaHostRegister(p, c->shm_bytes, cudaHostRegisterMapped | cudaHostRegisterPortable));
+    void* d = nullptr;
+    CK(cudaHostGetDevicePointer(&d, p, 0));
+    c->shm_dev[c->rank] = (char*)d;
+}
+
+void host_connect(jacobi3d* c) {  // map every neighbour rank's segment
+    for (int r : c->peer_ranks) {
+        const std::string nm = shm_name(c->job_key, r);
+        const int fd = shm_open(nm.c_str(), O_RDWR, 0600);
+        if (fd < 0) throw Error(J3D_EINVAL, "shm_open " + nm + " failed (ranks must share one node)");
+        void* p = mmap(nullptr, c->shm_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+        close(fd);
+        if (p == MAP_FAILED) throw Error(J3D_ENOMEM, "mmap of a neighbour's staging segment failed");
+        c->shm_base[r] = (char*)p;
+        CK(cudaHostRegister(p, c->shm_bytes, cudaHostRegisterMapped | cudaHostRegisterPortable));
+        void* d = nullptr;
+        CK(cudaHostGetDevicePointer(&d, p, 0));
+        c->shm_dev[r] = (char*)d;
+    }
+    c->host_connected = true;
+}
+
+void host_teardown(jacobi3d* c) {
+    for (size_t r = 0; r < c->shm_base.size(); ++r) {
+        if (!c->shm_base[r]) continue;
+        cudaHostUnregister(c->shm_base[r]);
+        munmap(c->shm_base[r], c->shm_bytes);
+        if ((int)r == c->rank) shm_unlink(shm_name(c->job_key, c->rank).c_str());
+        c->shm_base[r] = nullptr;
+    }
+}
+
+// Host-staged exchange of the PEER_HOST faces of parity par on stream st:
+// D2H of my send buffers into my segment, epoch signal into each neighbour's
+// segment flags, wait for theirs, H2D of their staging areas into my receive
+// buffers.  Flags: toggle protocol on slot (same rules as P2P, see p2p_sync).
+void host_exchange(jacobi3d* c, int par, int slot, cudaStream_t st) {
+    if (!c->host_needed) return;
+    const int n = c->n_gpus;
+    for (int l = 0; l < c->n_local; ++l)
+        for (int f = 0; f < 6; ++f)
+            if (c->kind[l][f] == PEER_HOST)
+                CK(cudaMemcpyAsync(c->shm_base[c->rank] + shm_area_offset(c, l, f, par),
+                                   c->face_buf(l, f, par, false), (size_t)face_cells(c->plan.ext, f) * 8,
+                                   cudaMemcpyDeviceToHost, st));
+    for (int r : c->peer_ranks)
+        DK(g_drv.write64((CUstream)st, (CUdeviceptr)((uint64_t*)c->shm_dev[r] + slot * n + c->rank), 1, 0));
+    for (int r : c->peer_ranks) {
+        CUdeviceptr f = (CUdeviceptr)((uint64_t*)c->shm_dev[c->rank] + slot * n + r);
+        DK(g_drv.wait64((CUstream)st, f, 1, CU_STREAM_WAIT_VALUE_EQ));
+        DK(g_drv.write64((CUstream)st, f, 0, 0));
+    }
+    for (int l = 0; l < c->n_local; ++l)
+        for (int f = 0; f < 6; ++f)
+            if (c->kind[l][f] == PEER_HOST) {
+                const int r = c->plan.blocks[c->plan.blocks[c->gid[l]].nbr[f]].owner;
+                CK(cudaMemcpyAsync(c->face_buf(l, f, par, true),
+                                   c->shm_base[r] + shm_area_offset(c, c->nbr_local[l][f], f ^ 1, par),
+                                   (size_t)face_cells(c->plan.ext, f) * 8, cudaMemcpyHostToDevice, st));
+            }
+}
+
+// epoch barrier through the host segments (refresh pre-barrier of the host backend)
+void host_sync(jacobi3d* c, int slot, cudaStream_t st) {
+    if (!c->host_needed) return;
+    const int n = c->n_gpus;
+    for (int r : c->peer_ranks)
+        DK(g_drv.write64((CUstream)st, (CUdeviceptr)((uint64_t*)c->shm_dev[r] + slot * n + c->rank), 1, 0));
+    for (int r : c->peer_ranks) {
+        CUdeviceptr f = (CUdeviceptr)((uint64_t*)c->shm_dev[c->rank] + slot * n + r);
+        DK(g_drv.wait64((CUstream)st, f, 1, CU_STREAM_WAIT_VALUE_EQ));
+        DK(g_drv.write64((CUstream)st, f, 0, 0));
+    }
+}
+
 void cross_gpu_exchange(jacobi3d* c, int par, int slot, cudaStream_t st) {
     if (c->n_gpus == 1 || c->skip_exchange) return;
     nccl_exchange(c, par, st);
     p2p_sync(c, slot, st);
+    host_exchange(c, par, slot, st);
 }
 
 // Full halo refresh of buffer parity `par`: pack, exchange, unpack, batched on
@@ -687,11 +816,15 @@ void cross_gpu_exchange(jacobi3d* c, int par, int slot, cudaStream_t st) {
 void refresh(jacobi3d* c, int par) {
     const int rc = (int)(c->refresh_count & 1);
     c->refresh_count++;
-    if (c->n_gpus > 1) p2p_sync(c, 4 + rc, c->main);
+    if (c->n_gpus > 1) {
+        p2p_sync(c, 4 + rc, c->main);
+        host_sync(c, 4 + rc, c->main);
+    }
     copies(c, c->d_pack, par, -1, 0, true, c->main);
     if (c->n_gpus > 1) {
         nccl_exchange(c, par, c->main);
         p2p_sync(c, 2 + rc, c->main);
+        host_exchange(c, par, 2 + rc, c->main);
     }
     copies(c, c->d_unpack, par, -1, 0, true, c->main);
 }
@@ -891,6 +1024,7 @@ void destroy_ctx(jacobi3d* c) {
     if (c->comm) ncclCommDestroy(c->comm);
     for (size_t r = 0; r < c->peer_base.size(); ++r)
         if (c->peer_base[r]) cudaIpcCloseMemHandle(c->peer_base[r]);
+    host_teardown(c);
     if (c->main) cudaStreamDestroy(c->main);
     cudaFree(c->d_descs);
     cudaFree(c->d_tmaps);
@@ -1056,6 +1190,13 @@ int jacobi3d_create(const jacobi3d_config* cfg, const uint8_t* nccl_uid, jacobi3
             ncclUniqueId id;
             std::memcpy(&id, nccl_uid, 128);
             NK(ncclCommInitRank(&c->comm, c->n_gpus, id, c->rank));
+            uint64_t h = 1469598103934665603ULL;  // FNV-1a of the unique id: a job-wide key
+            for (int i = 0; i < 128; ++i) h = (h ^ nccl_uid[i]) * 1099511628211ULL;
+            c->job_key = h;
+        }
+        if (c->host_needed) {
+            g_drv.load();
+            host_setup_own(c);
         }
         CK(cudaDeviceSynchronize());
         *out = c;
@@ -1090,6 +1231,10 @@ int jacobi3d_ipc_export(jacobi3d_t* c, uint8_t* host_out, size_t cap, size_t* le
 int jacobi3d_ipc_connect(jacobi3d_t* c, const uint8_t* all, size_t len_per_rank) {
     return guarded([&]() -> int {
         if (!c || !all) return fail(J3D_EINVAL, "NULL argument");
+        if (c->host_needed && !c->host_connected) {
+            CK(cudaSetDevice(c->device));
+            host_connect(c);
+        }
         if (!c->p2p_needed) return J3D_OK;
         if (len_per_rank != sizeof(IpcRecord)) return fail(J3D_EINVAL, "record size mismatch");
         CK(cudaSetDevice(c->device));
@@ -1120,8 +1265,8 @@ int jacobi3d_init(jacobi3d_t* c, int kind, const double* p, uint64_t seed) {
         if (!c) return fail(J3D_EINVAL, "ctx is NULL");
         if (kind < J3D_INIT_DEFAULT || kind > J3D_INIT_HASH) return fail(J3D_EINVAL, "unknown init kind");
         if ((kind == J3D_INIT_CONST || kind == J3D_INIT_LINEAR) && !p) return fail(J3D_EINVAL, "params required");
-        if (c->p2p_needed && !c->p2p_connected)
-            return fail(J3D_ESTATE, "P2P exchange needs jacobi3d_ipc_export/jacobi3d_ipc_connect first");
+        if ((c->p2p_needed && !c->p2p_connected) || (c->host_needed && !c->host_connected))
+            return fail(J3D_ESTATE, "P2P / host exchange needs jacobi3d_ipc_export/jacobi3d_ipc_connect first");
         CK(cudaSetDevice(c->device));
         double pp[4] = {0, 0, 0, 0};
         if (p) std::memcpy(pp, p, sizeof pp);

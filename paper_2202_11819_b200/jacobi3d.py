@@ -21,8 +21,8 @@ UNFUSED, FUSE_A, FUSE_B, FUSE_C, FUSE_DIRECT = 0, 1, 2, 3, 4
 VARIANTS = {"unfused": UNFUSED, "A": FUSE_A, "B": FUSE_B, "C": FUSE_C, "direct": FUSE_DIRECT}
 PER_BLOCK, BATCHED = 0, 1
 LAUNCHES = {"per_block": PER_BLOCK, "batched": BATCHED}
-XCHG_AUTO, XCHG_NCCL, XCHG_P2P = 0, 1, 2
-EXCHANGES = {"auto": XCHG_AUTO, "nccl": XCHG_NCCL, "p2p": XCHG_P2P}
+XCHG_AUTO, XCHG_NCCL, XCHG_P2P, XCHG_HOST = 0, 1, 2, 3
+EXCHANGES = {"auto": XCHG_AUTO, "nccl": XCHG_NCCL, "p2p": XCHG_P2P, "host": XCHG_HOST}
 INIT_DEFAULT, INIT_CONST, INIT_LINEAR, INIT_HASH = 0, 1, 2, 3
 INITS = {"default": INIT_DEFAULT, "const": INIT_CONST, "linear": INIT_LINEAR, "hash": INIT_HASH}
 

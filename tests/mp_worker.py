@@ -77,11 +77,17 @@ def main():
                                                       [False, True]):
         cases.append((g, 4, variant, "batched", graph, exchange, 7, "hash", 2, True))
         cases.append((g, 1, variant, "batched", graph, exchange, 5, "hash", 2, True))
+    # host-staged exchange (the paper's -H versions)
+    for variant, launch, graph in itertools.product(["direct", "C", "unfused"], ["batched", "per_block"],
+                                                    [False, True]):
+        cases.append((g, 4, variant, launch, graph, "host", 6, "hash", 4))
+    cases.append((gx, 2, "direct", "batched", False, "host", 6, "hash", 4, True))
     cases.append(((45, 34, 44), 2, "direct", "batched", False, "p2p", 7, "hash", 1))
     cases.append(((45, 34, 44), 2, "C", "per_block", False, "nccl", 7, "hash", 1))
     if which == "debug":
         cases = [((16, 8, 16), 1, "direct", "batched", False, "p2p", n_, "hash", 3) for n_ in (0, 1, 2, 3)]
         cases += [((16, 8, 16), 1, v, "batched", False, "p2p", 2, "hash", 3) for v in ("unfused", "C")]
+        cases += [((16, 8, 16), 1, v, "batched", False, "host", 2, "hash", 3) for v in ("unfused", "direct")]
     n, failed = 0, []
     for c in cases:
         try:
