@@ -467,10 +467,11 @@ void build_static_tables(jacobi3d* c) {
     const int nl = c->n_local;
     // ---- tensor maps [2*l + p] over each input buffer
     g_drv.load();
-    // 128x30 tiles (15 consumer warps, 5-stage ring, 1 CTA/SM) for wide
-    // blocks, 64x16 tiles (3 CTAs/SM) for narrow ones; both read every value
-    // from shared memory (no register carry).  Bench sweeps: profiles/, DESIGN.md.
-    c->tile_kind = c->nx >= 128 ? 16 : 17;
+    // 192x22 tiles (11 consumer warps, 5-stage ring, 1 CTA/SM) when they divide
+    // the block width, else 128x30 (15 consumer warps) for wide blocks and
+    // 64x16 (3 CTAs/SM) for narrow ones; all read every value from shared
+    // memory (no register carry).  Bench sweeps: profiles/, DESIGN.md.
+    c->tile_kind = (c->nx % 192 == 0) ? 19 : c->nx >= 128 ? 16 : (c->nx > 64 && c->ny % 24 == 0) ? 21 : 17;
     if (const char* e = std::getenv("J3D_TILE")) {  // tuning override (bench sweeps)
         const int k = std::atoi(e);
         if (k >= 0 && k < num_tile_kinds()) c->tile_kind = k;
@@ -515,6 +516,8 @@ void build_static_tables(jacobi3d* c) {
         const int64_t L = std::atoll(e);
         if (L > 0) best_zc = std::max<int64_t>(1, (c->nz + L - 1) / L);
     }
+    int tile_order = 0;  // tuning override: tile order inside a z chunk
+    if (const char* e = std::getenv("J3D_TILE_ORDER")) tile_order = std::atoi(e);
     std::vector<WorkItem> items;
     c->item_begin.assign(nl, 0);
     c->item_count.assign(nl, 0);
@@ -530,8 +533,20 @@ void build_static_tables(jacobi3d* c) {
         for (int64_t zc = 0; zc < best_zc; ++zc) {
             const int z0 = (int)(c->nz * zc / best_zc), z1 = (int)(c->nz * (zc + 1) / best_zc);
             if (z1 <= z0) continue;
-            for (int64_t ty = 0; ty < nty; ++ty)
-                for (int64_t tx = 0; tx < ntx; ++tx) items.push_back(WorkItem{l, (int16_t)tx, (int16_t)ty, z0, z1});
+            if (tile_order == 1) {  // y fastest
+                for (int64_t tx = 0; tx < ntx; ++tx)
+                    for (int64_t ty = 0; ty < nty; ++ty)
+                        items.push_back(WorkItem{l, (int16_t)tx, (int16_t)ty, z0, z1});
+            } else if (tile_order >= 2) {  // bands of `tile_order` tile rows, column-major inside a band
+                for (int64_t b0 = 0; b0 < nty; b0 += tile_order)
+                    for (int64_t tx = 0; tx < ntx; ++tx)
+                        for (int64_t ty = b0; ty < std::min<int64_t>(nty, b0 + tile_order); ++ty)
+                            items.push_back(WorkItem{l, (int16_t)tx, (int16_t)ty, z0, z1});
+            } else {  // x fastest
+                for (int64_t ty = 0; ty < nty; ++ty)
+                    for (int64_t tx = 0; tx < ntx; ++tx)
+                        items.push_back(WorkItem{l, (int16_t)tx, (int16_t)ty, z0, z1});
+            }
         }
         c->item_count[l] = (int)items.size() - c->item_begin[l];
     }

@@ -379,10 +379,17 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
         // from the same inputs and store again / store the face values.
         // st: stage of plane z (+ this thread's offset); CC/ZM/ZP give the
         // centre values of planes z, z-1, z+1 for cell pair (r, c).
-        auto compute_plane_t = [&](auto faces_tag, int z, uint32_t fm, const double* st, auto&& CC, auto&& ZM,
+        auto compute_plane_t = [&](auto mode_tag, int z, uint32_t fm, const double* st, auto&& CC, auto&& ZM,
                                    auto&& ZP) {
-            constexpr bool FACES = decltype(faces_tag)::value;
+            // MODE 0: no face work; 1: x faces only (values captured in the hot
+            // loop, stored by the owning lane afterwards); 2: any faces, inline
+            constexpr int MODE = decltype(mode_tag)::value;
+            constexpr bool FACES = MODE == 2;
             double* op = obase + (int64_t)(z + 1) * zs;
+            double cap0[RPW], cap1[RPW];  // MODE 1: new values of the x = 0 / x = nx-1 cells of each row
+            const int xlast = nx - 1 - x0;  // tile-local x of the last cell
+            const int clast = xlast >> 6, lane_last = (xlast & 63) >> 1;
+            const bool last_is_x = !(xlast & 1);
             // Fused epilogue ("pack fused into the update"): faces this plane
             // feeds are stored inline next to the output -- z faces (the whole
             // plane) and y faces (whole rows) as 16-byte stores where aligned,
@@ -436,6 +443,10 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                     const double s1 = sum7(cc.y, cc.x, p[2], ym.y, yp.y, ZM(r, c).y, ZP(r, c).y);
                     tiny |= (fabs(s0) < kDiv7Tiny) | (fabs(s1) < kDiv7Tiny);
                     const double vx = div7_fast(s0), vy = div7_fast(s1);
+                    if constexpr (MODE == 1) {
+                        if (c == 0) cap0[r] = vx;
+                        if (c == clast) cap1[r] = last_is_x ? vx : vy;
+                    }
                     double* o = op + r * pitch + 64 * c;
                     const int x = xl + 64 * c, y = yl + r;
                     const bool v1 = whole || (y < ny && x + 1 < nx);
@@ -472,6 +483,22 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                     }
                 }
             }
+            if constexpr (MODE == 1) {
+                if ((fm & 1u) && x0 == 0 && lane == 0) {
+                    const FaceRef F = load_face(&d->epi[0]);
+                    double* q = F.p + (int64_t)z * F.sb;
+#pragma unroll
+                    for (int r = 0; r < RPW; ++r)
+                        if (yl + r < ny) q[(int64_t)(yl + r) * F.sa] = cap0[r];
+                }
+                if ((fm & 2u) && clast < CPL && lane == lane_last) {
+                    const FaceRef F = load_face(&d->epi[1]);
+                    double* q = F.p + (int64_t)z * F.sb;
+#pragma unroll
+                    for (int r = 0; r < RPW; ++r)
+                        if (yl + r < ny) q[(int64_t)(yl + r) * F.sa] = cap1[r];
+                }
+            }
             if (tiny || (FACES && rare_faces)) {
 #pragma unroll
                 for (int r = 0; r < RPW; ++r) {
@@ -502,8 +529,9 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
         // epilogue code at all
         auto compute_plane = [&](int z, const double* st, auto&& CC, auto&& ZM, auto&& ZP) {
             const uint32_t fm = epi & (touch | (z == 0 ? 16u : 0u) | (z == nz - 1 ? 32u : 0u));
-            if (fm) compute_plane_t(std::true_type{}, z, fm, st, CC, ZM, ZP);
-            else compute_plane_t(std::false_type{}, z, 0u, st, CC, ZM, ZP);
+            if (fm & ~3u) compute_plane_t(std::integral_constant<int, 2>{}, z, fm, st, CC, ZM, ZP);
+            else if (fm) compute_plane_t(std::integral_constant<int, 1>{}, z, fm, st, CC, ZM, ZP);
+            else compute_plane_t(std::integral_constant<int, 0>{}, z, 0u, st, CC, ZM, ZP);
         };
 
         int scur;
@@ -715,7 +743,10 @@ cudaError_t launch_div7_selftest(uint64_t n, uint64_t seed, unsigned long long* 
     X(15, 64, 8, 2, 6, 2, 0)    /* 64x16 from smem only                        */ \
     X(16, 128, 15, 2, 5, 1, 0)  /* 128x30 from smem only, 5 stages             */ \
     X(17, 64, 8, 2, 7, 3, 0)    /* 64x16 from smem only, 3 CTAs/SM             */ \
-    X(18, 128, 8, 1, 8, 2, 0)   /* 128x8 from smem only, 8 stages              */
+    X(18, 128, 8, 1, 8, 2, 0)   /* 128x8 from smem only, 8 stages              */ \
+    X(19, 192, 11, 2, 5, 1, 0)  /* 192x22 from smem only, 5 x 37.6 KB          */ \
+    X(20, 192, 15, 2, 4, 1, 0)  /* 192x30 from smem only, 4 x 50 KB            */ \
+    X(21, 128, 12, 2, 5, 1, 0)  /* 128x24 from smem only (96-wide blocks)     */
 
 template <class T>
 static cudaError_t launch_t(const StencilLaunch& L, cudaStream_t st) {
@@ -743,7 +774,7 @@ static cudaError_t occ_t(int* blocks) {
 
 #define J3D_TYPE(k, tx, ncw, rpw, ns, mb, cy) Tile<tx, ncw, rpw, ns, mb, cy>
 
-int num_tile_kinds() { return 19; }
+int num_tile_kinds() { return 22; }
 
 TileShape tile_shape(int kind) {
     switch (kind) {
