@@ -471,7 +471,7 @@ void build_static_tables(jacobi3d* c) {
     // the block width, else 128x30 (15 consumer warps) for wide blocks and
     // 64x16 (3 CTAs/SM) for narrow ones; all read every value from shared
     // memory (no register carry).  Bench sweeps: profiles/, DESIGN.md.
-    c->tile_kind = (c->nx % 192 == 0) ? 19 : c->nx >= 128 ? 16 : (c->nx > 64 && c->ny % 24 == 0) ? 21 : 17;
+    c->tile_kind = (c->nx % 192 == 0) ? 19 : c->nx >= 128 ? 16 : 17;
     if (const char* e = std::getenv("J3D_TILE")) {  // tuning override (bench sweeps)
         const int k = std::atoi(e);
         if (k >= 0 && k < num_tile_kinds()) c->tile_kind = k;
