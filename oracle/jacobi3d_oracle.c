@@ -82,6 +82,8 @@ void oracle_set_threads(int n) {
 void oracle_init(int64_t gx, int64_t gy, int64_t gz, int kind, const double *p,
                  uint64_t seed, double boundary, double *U) {
     const uint64_t s = oracle_splitmix64(seed);
+    /* planes are independent: OpenMP cannot change any value */
+#pragma omp parallel for schedule(static)
     for (int64_t k = -1; k <= gz; ++k)
         for (int64_t j = -1; j <= gy; ++j)
             for (int64_t i = -1; i <= gx; ++i) {

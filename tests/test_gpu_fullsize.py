@@ -69,3 +69,20 @@ def test_weak_1536_fixed_point_at_scale():
         ctx.iterate(10)
         assert ctx.checksum() == c0
         assert ctx.residual() == 0.0
+
+
+def test_weak_1536_checksum_vs_full_oracle():
+    """The whole 1536^3 grid after 3 iterations (bench.py's configuration):
+    the GPU checksum equals the checksum of the CPU oracle run on the same
+    hash input (needs ~60 GB of host RAM; the GPU box has 196 GB)."""
+    from oracle import core
+
+    grid = (1536, 1536, 1536)
+    with j3d.Jacobi3D(grid, odf=1, variant="direct", launch="batched") as ctx:
+        ctx.init("hash", seed=SEED)
+        ctx.iterate(3)
+        got = ctx.checksum()
+    U = core.init(*grid, core.INIT_HASH, seed=SEED)
+    R = core.run(U, 3)
+    del U
+    assert got == core.checksum(R)
