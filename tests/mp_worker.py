@@ -52,6 +52,51 @@ def run_case(grid, odf, variant, launch, graph, exchange, n, kind, seed, overlap
         ctx.close()
 
 
+def run_fullsize(world):
+    """bench.py's weak-scaling configuration at full size (1536^3 per GPU):
+    sampled cells on both sides of every inter-GPU face (and random ones) are
+    compared bit for bit with the oracle evaluated on their dependency cones."""
+    from tests.helpers import cone_value
+
+    grids = {1: (1536, 1536, 1536), 2: (1536, 1536, 3072), 4: (1536, 3072, 3072)}
+    grid = grids[world]
+    seed, n = 20220223, 3
+    rank = dist.get_rank()
+    rng = np.random.default_rng(100 + rank)
+    checked = 0
+    for odf, variant, exchange in ((1, "direct", "p2p"), (8, "unfused", "nccl")):
+        ctx = jdist.create(grid, odf=odf, variant=variant, exchange=exchange)
+        try:
+            ctx.init("hash", seed=seed)
+            ctx.iterate(n)
+            ctx.synchronize()
+            gpu_grid = ctx.plan["gpu_grid"]
+            per = [g // p for g, p in zip(grid, gpu_grid)]
+            mine = [b for b in range(ctx.n_blocks) if ctx.block_info(b)[2] == rank]
+            for b in mine:
+                (ox, oy, oz), (ex, ey, ez), _ = ctx.block_info(b)
+                cells = []
+                for a in range(3):  # both sides of GPU boundaries inside / next to this block
+                    lo, hi = (ox, oy, oz)[a], (ox, oy, oz)[a] + (ex, ey, ez)[a]
+                    for side in (lo, hi - 1):
+                        if side % per[a] in (0, per[a] - 1):
+                            c = [int(rng.integers(ox, ox + ex)), int(rng.integers(oy, oy + ey)),
+                                 int(rng.integers(oz, oz + ez))]
+                            c[a] = side
+                            cells.append(tuple(c))
+                for _ in range(3):
+                    cells.append((int(rng.integers(ox, ox + ex)), int(rng.integers(oy, oy + ey)),
+                                  int(rng.integers(oz, oz + ez))))
+                for (i, j, k) in cells:
+                    got = ctx.get_region(b, (i - ox, j - oy, k - oz), (1, 1, 1))[0, 0, 0]
+                    want = cone_value(grid, seed, n, (i, j, k))
+                    assert np.float64(got).tobytes() == np.float64(want).tobytes(), (rank, odf, (i, j, k), got, want)
+                    checked += 1
+        finally:
+            ctx.close()
+    return checked
+
+
 def main():
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
@@ -84,6 +129,12 @@ def main():
     cases.append((gx, 2, "direct", "batched", False, "host", 6, "hash", 4, True))
     cases.append(((45, 34, 44), 2, "direct", "batched", False, "p2p", 7, "hash", 1))
     cases.append(((45, 34, 44), 2, "C", "per_block", False, "nccl", 7, "hash", 1))
+    if which == "fullsize":
+        k = run_fullsize(world)
+        dist.barrier()
+        print(f"MP OK fullsize: rank {dist.get_rank()} checked {k} sampled cells", flush=True)
+        dist.destroy_process_group()
+        return
     if which == "debug":
         cases = [((16, 8, 16), 1, "direct", "batched", False, "p2p", n_, "hash", 3) for n_ in (0, 1, 2, 3)]
         cases += [((16, 8, 16), 1, v, "batched", False, "p2p", 2, "hash", 3) for v in ("unfused", "C")]

@@ -33,3 +33,14 @@ def test_multi_gpu_parity():
            os.path.join(ROOT, "tests", "mp_worker.py"), os.environ.get("J3D_MP_CASES", "quick")]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert p.returncode == 0 and "MP OK" in p.stdout, p.stdout[-3000:] + p.stderr[-5000:]
+
+
+@pytest.mark.skipif(gpu_count() < 2, reason="needs >= 2 GPUs")
+def test_multi_gpu_fullsize_sampled():
+    """Weak scaling at bench.py's full size (1536^3 per GPU), sampled parity."""
+    n = 4 if gpu_count() >= 4 else 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "tests", "mp_worker.py"), "fullsize"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT)
+    assert p.returncode == 0 and "MP OK fullsize" in p.stdout, p.stdout[-3000:] + p.stderr[-5000:]
