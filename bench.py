@@ -304,6 +304,22 @@ def e2e_run(ctx, grid, a, world, rank):
     ex = ctx.extent
     blocks = [b for b in range(ctx.n_blocks) if ctx.block_info(b)[2] == ctx.cfg.rank]
     nb = ex[0] * ex[1] * ex[2]
+    # every rank on this node pins its whole field: only if it fits comfortably in host RAM
+    need = 8 * nb * len(blocks) * int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    avail = 0
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    avail = int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    ok = torch.tensor([1.0 if need <= 0.45 * avail else 0.0], device="cuda")
+    if world > 1:
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if ok.item() < 1.0:
+        return {"value": None, "unit": "GLUPS", "skipped": f"pinned host copies of the field need {need/1e9:.0f} GB, "
+                f"MemAvailable {avail/1e9:.0f} GB on this node"}
     host = torch.empty(nb * len(blocks), dtype=torch.float64, pin_memory=True)
     hp = host.data_ptr()
     # synthetic initial field on the host (uniform [0,1), not timed)

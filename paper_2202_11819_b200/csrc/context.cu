@@ -144,6 +144,8 @@ struct jacobi3d {
     // device tables
     StencilDesc* d_descs = nullptr;
     CUtensorMap* d_tmaps = nullptr;
+    CUtensorMap* d_tmaps_split = nullptr;
+    int tma_mode = 0;
     WorkItem* d_items = nullptr;
     CopyDesc* d_pack = nullptr;
     CopyDesc* d_unpack = nullptr;
@@ -495,6 +497,23 @@ void build_static_tables(jacobi3d* c) {
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
         }
     CK(cudaMemcpy(c->d_tmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+    // split maps: box heights 2 and H-4 (for the L2-policy split loads)
+    std::vector<CUtensorMap> maps2(4 * nl);
+    for (int l = 0; l < nl; ++l)
+        for (int p = 0; p < 2; ++p)
+            for (int h = 0; h < 2; ++h) {
+                cuuint64_t dims[3] = {(cuuint64_t)c->pitch, (cuuint64_t)(c->ny + 2), (cuuint64_t)(c->nz + 2)};
+                cuuint64_t strides[2] = {(cuuint64_t)(c->pitch * 8), (cuuint64_t)(c->zs * 8)};
+                const int H = stencil_box_h(c->tile_kind);
+                cuuint32_t box[3] = {(cuuint32_t)stencil_box_w(c->tile_kind), (cuuint32_t)(h == 0 ? 2 : std::max(1, H - 4)), 1};
+                cuuint32_t es[3] = {1, 1, 1};
+                DK(g_drv.encode(&maps2[(2 * l + p) * 2 + h], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->buf(l, p), dims,
+                                strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+            }
+    CK(cudaMemcpy(c->d_tmaps_split, maps2.data(), maps2.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+    if (const char* e = std::getenv("J3D_TMA_HINT")) c->tma_mode = std::atoi(e) & 3;
+    if (c->tma_mode == 3 && stencil_box_h(c->tile_kind) < 6) c->tma_mode = 0;
 
     // ---- work items: per block, z-chunk outer, then ty, tx (x fastest), peer-face blocks first
     int occ = 1;
@@ -611,6 +630,8 @@ void stencil(jacobi3d* c, int begin, int count, int parity, cudaStream_t st, int
     StencilLaunch L;
     L.descs = c->d_descs;
     L.tmaps = c->d_tmaps;
+    L.tmaps_split = c->d_tmaps_split;
+    L.tma_mode = c->tma_mode;
     L.items = c->d_items + begin;
     L.n_items = count;
     L.parity = parity;
@@ -1043,6 +1064,7 @@ void destroy_ctx(jacobi3d* c) {
     if (c->main) cudaStreamDestroy(c->main);
     cudaFree(c->d_descs);
     cudaFree(c->d_tmaps);
+    cudaFree(c->d_tmaps_split);
     cudaFree(c->d_items);
     cudaFree(c->d_pack);
     cudaFree(c->d_unpack);
@@ -1155,6 +1177,7 @@ int jacobi3d_create(const jacobi3d_config* cfg, const uint8_t* nccl_uid, jacobi3
         CK(cudaMemset(c->arena + c->off_faces, 0, (size_t)(c->arena_bytes - c->off_faces)));
         CK(cudaMalloc(&c->d_descs, sizeof(StencilDesc) * 2 * c->n_local));
         CK(cudaMalloc(&c->d_tmaps, sizeof(CUtensorMap) * 2 * c->n_local));
+        CK(cudaMalloc(&c->d_tmaps_split, sizeof(CUtensorMap) * 4 * c->n_local));
         CK(cudaMalloc(&c->d_pack, sizeof(CopyDesc) * 12 * c->n_local));
         CK(cudaMalloc(&c->d_unpack, sizeof(CopyDesc) * 12 * c->n_local));
         CK(cudaMalloc(&c->d_unpack_nccl, sizeof(CopyDesc) * 12 * c->n_local));

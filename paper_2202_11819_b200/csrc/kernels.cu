@@ -66,6 +66,14 @@ __device__ __forceinline__ void tmap_acquire(const CUtensorMap* m) {
     asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(reinterpret_cast<uint64_t>(m))
                  : "memory");
 }
+__device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2,
+                                                 uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
@@ -151,7 +159,9 @@ struct Tile {
     static constexpr bool CARRY = CARRY_ != 0;
     static constexpr int TY = NCW * RPW;
     static constexpr int CPL = TX / 64;
-    static constexpr int W = TX + 4;  // smem row: x0-2 .. x0+TX+1 (16-B aligned interior)
+    static constexpr int HX = 4;      // halo columns kept left of the tile in smem
+    static constexpr int W = TX + 2 * HX;  // smem row: x0-4 .. x0+TX+3: the same 32-B sectors as x0-1 .. x0+TX,
+                                           // 16-B aligned interior, rows a multiple of 64 B
     static constexpr int H = TY + 2;  // y0-1 .. y0+TY
     static constexpr uint32_t TX_BYTES = W * H * 8;
     static constexpr int STAGE_BYTES = (W * H * 8 + 127) / 128 * 128;
@@ -181,7 +191,7 @@ __device__ __forceinline__ void patch_stage(const StencilDesc* __restrict__ d, d
             if (y >= ny) break;
             for (int lx = lane; lx < T::TX; lx += 32) {
                 const int x = x0 + lx;
-                if (x < nx) st[(r0 + r + 1) * W + lx + 2] = F.p[x * F.sa + y * F.sb];
+                if (x < nx) st[(r0 + r + 1) * W + lx + T::HX] = F.p[x * F.sa + y * F.sb];
             }
         }
         return;
@@ -190,7 +200,7 @@ __device__ __forceinline__ void patch_stage(const StencilDesc* __restrict__ d, d
         const FaceRef F = load_face(&d->pro[2]);
         for (int lx = lane; lx < T::TX; lx += 32) {
             const int x = x0 + lx;
-            if (x < nx) st[lx + 2] = F.p[x * F.sa + zz * F.sb];
+            if (x < nx) st[lx + T::HX] = F.p[x * F.sa + zz * F.sb];
         }
     }
     if (pro & 8u) {
@@ -199,7 +209,7 @@ __device__ __forceinline__ void patch_stage(const StencilDesc* __restrict__ d, d
             const FaceRef F = load_face(&d->pro[3]);
             for (int lx = lane; lx < T::TX; lx += 32) {
                 const int x = x0 + lx;
-                if (x < nx) st[(gl + 1) * W + lx + 2] = F.p[x * F.sa + zz * F.sb];
+                if (x < nx) st[(gl + 1) * W + lx + T::HX] = F.p[x * F.sa + zz * F.sb];
             }
         }
     }
@@ -208,13 +218,13 @@ __device__ __forceinline__ void patch_stage(const StencilDesc* __restrict__ d, d
         if (y < ny) {
             if ((pro & 1u) && x0 == 0) {
                 const FaceRef F = load_face(&d->pro[0]);
-                st[(r0 + lane + 1) * W + 1] = F.p[y * F.sa + zz * F.sb];
+                st[(r0 + lane + 1) * W + T::HX - 1] = F.p[y * F.sa + zz * F.sb];
             }
             if (pro & 2u) {
                 const int gx = nx - x0;  // tile-local x of the +x ghost
                 if (gx <= T::TX + 1) {
                     const FaceRef F = load_face(&d->pro[1]);
-                    st[(r0 + lane + 1) * W + gx + 2] = F.p[y * F.sa + zz * F.sb];
+                    st[(r0 + lane + 1) * W + gx + T::HX] = F.p[y * F.sa + zz * F.sb];
                 }
             }
         }
@@ -264,8 +274,8 @@ __device__ __forceinline__ void epi_store(const StencilDesc* __restrict__ d, uin
 template <class T>
 __global__ void __launch_bounds__(T::THREADS, T::MINB)
     stencil_tma_kernel(const StencilDesc* __restrict__ descs, const CUtensorMap* __restrict__ tmaps,
-                       const WorkItem* __restrict__ items, int n_items, int parity, int flags,
-                       unsigned int* __restrict__ sched) {
+                       const CUtensorMap* __restrict__ tmaps3, const WorkItem* __restrict__ items, int n_items,
+                       int parity, int flags, unsigned int* __restrict__ sched) {
     constexpr int NCW = T::NCW, RPW = T::RPW, CPL = T::CPL, W = T::W, NSTAGE = T::NSTAGE, IQ = 4;
     // The kernel has no static shared memory, so the dynamic window starts at
     // shared offset 0 (1024-B aligned); indexing the __shared__ array directly
@@ -296,6 +306,10 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
         if (lane == 0) {
             int s = 0, qs = 0;
             uint32_t ph = 0, qph = 0;
+            const int tma_mode = (flags >> 2) & 3;
+            uint64_t pol_first = 0, pol_last = 0;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
             for (;;) {
                 int it = (int)atomicAdd(&sched[0], 1u);
                 if (it >= n_items) it = -1;
@@ -307,11 +321,23 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                 const WorkItem w = items[it];
                 const CUtensorMap* tm = tmaps + (2 * w.blk + parity);
                 tmap_acquire(tm);
-                const int c0 = XOFF + w.tx * T::TX - 2, c1 = w.ty * T::TY;
+                const int c0 = XOFF + w.tx * T::TX - T::HX, c1 = w.ty * T::TY;
                 for (int z = w.z0 - 1; z <= w.z1; ++z) {
                     mbar_wait(&empty[s], ph ^ 1);
                     mbar_expect_tx(&full[s], T::TX_BYTES);
-                    tma_load_3d(smem + s * T::STAGE_BYTES, tm, &full[s], c0, c1, z + 1);
+                    unsigned char* dst = smem + s * T::STAGE_BYTES;
+                    if (tma_mode == 0) {
+                        tma_load_3d(dst, tm, &full[s], c0, c1, z + 1);
+                    } else if (tma_mode == 1 || tma_mode == 2) {
+                        tma_load_3d_hint(dst, tm, &full[s], c0, c1, z + 1, tma_mode == 1 ? pol_first : pol_last);
+                    } else {
+                        // the two rows at each end of the box are shared with the
+                        // y-neighbour tiles: keep them (evict_last); stream the rest
+                        const CUtensorMap* t2 = tmaps3 + 2 * (2 * w.blk + parity);
+                        tma_load_3d_hint(dst, t2, &full[s], c0, c1, z + 1, pol_last);
+                        tma_load_3d_hint(dst + 2 * T::W * 8, t2 + 1, &full[s], c0, c1 + 2, z + 1, pol_first);
+                        tma_load_3d_hint(dst + (T::H - 2) * T::W * 8, t2, &full[s], c0, c1 + T::H - 2, z + 1, pol_last);
+                    }
                     if (++s == NSTAGE) { s = 0; ph ^= 1; }
                 }
             }
@@ -355,7 +381,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
         const uint32_t touch = (x0 == 0 ? 1u : 0u) | (x0 + T::TX >= nx ? 2u : 0u) | (y0 == 0 ? 4u : 0u) |
                                (y0 + T::TY >= ny ? 8u : 0u);
         const bool whole = x0 + T::TX <= nx && y0 + T::TY <= ny;  // no cell of the tile is outside the block
-        const int sbase = (warp * RPW + 1) * W + 2 * lane + 2;  // smem offset of cell (r = 0, c = 0)
+        const int sbase = (warp * RPW + 1) * W + 2 * lane + T::HX;  // smem offset of cell (r = 0, c = 0)
 
         // wait for the stage of plane zz, patch its ghosts (fused prologue) if needed
         auto acquire = [&](int zz) {
@@ -758,9 +784,9 @@ static cudaError_t launch_t(const StencilLaunch& L, cudaStream_t st) {
         attr_set = true;
     }
     if (L.n_items <= 0) return cudaSuccess;
-    stencil_tma_kernel<T><<<L.grid, T::THREADS, T::SMEM_BYTES, st>>>(L.descs, L.tmaps, L.items, L.n_items, L.parity,
-                                                                     (L.faces ? 1 : 0) | (L.store_hint ? 2 : 0),
-                                                                     L.sched);
+    stencil_tma_kernel<T><<<L.grid, T::THREADS, T::SMEM_BYTES, st>>>(
+        L.descs, L.tmaps, L.tmaps_split, L.items, L.n_items, L.parity,
+        (L.faces ? 1 : 0) | (L.store_hint ? 2 : 0) | ((L.tma_mode & 3) << 2), L.sched);
     return cudaGetLastError();
 }
 
@@ -806,7 +832,7 @@ cudaError_t stencil_occupancy(int kind, bool, int* blocks_per_sm) {
     return cudaErrorInvalidValue;
 }
 
-int stencil_box_w(int kind) { return tile_shape(kind).tx + 4; }
+int stencil_box_w(int kind) { return tile_shape(kind).tx + 8; }
 int stencil_box_h(int kind) { return tile_shape(kind).ty + 2; }
 
 cudaError_t launch_copy_faces(const CopyDesc* d, int per_group, int groups, int64_t max_cells, cudaStream_t st) {
