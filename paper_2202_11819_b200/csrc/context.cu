@@ -471,9 +471,8 @@ void build_static_tables(jacobi3d* c) {
     g_drv.load();
     // 192x22 tiles (11 consumer warps, 5-stage ring, 1 CTA/SM) when they divide
     // the block width, else 128x30 (15 consumer warps) for wide blocks and
-    // 64x16 (3 CTAs/SM) for narrow ones; all read every value from shared
-    // memory (no register carry).  Bench sweeps: profiles/, DESIGN.md.
-    c->tile_kind = (c->nx % 192 == 0) ? 19 : c->nx >= 128 ? 16 : 17;
+    // 64x16 (2 CTAs/SM, 6 stages) for narrow ones.  Bench sweeps: profiles/.
+    c->tile_kind = (c->nx % 192 == 0) ? 0 : c->nx >= 128 ? 1 : 4;
     if (const char* e = std::getenv("J3D_TILE")) {  // tuning override (bench sweeps)
         const int k = std::atoi(e);
         if (k >= 0 && k < num_tile_kinds()) c->tile_kind = k;

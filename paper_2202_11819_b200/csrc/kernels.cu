@@ -95,6 +95,10 @@ __device__ __forceinline__ FaceRef load_face(const FaceRef* f) {
     return r;
 }
 
+__device__ __forceinline__ void st_global_v2(double* p, double a, double b) {
+    asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
+
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     uint64_t z = x + 0x9E3779B97F4A7C15ULL;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -150,13 +154,9 @@ __device__ __forceinline__ double sum7(double c, double xm, double xp, double ym
 // Tile shape: TX cells along x (a warp covers 64 with double2 per lane, CPL
 // column groups), NCW consumer warps each owning RPW rows (TY = NCW*RPW),
 // NSTAGE plane buffers in the TMA ring, MINB CTAs per SM targeted.
-template <int TX_, int NCW_, int RPW_, int NSTAGE_, int MINB_, int CARRY_ = 1>
+template <int TX_, int NCW_, int RPW_, int NSTAGE_, int MINB_>
 struct Tile {
     static constexpr int TX = TX_, NCW = NCW_, RPW = RPW_, NSTAGE = NSTAGE_, MINB = MINB_;
-    // CARRY: the centre values of planes z-1, z, z+1 live in registers (three
-    // sets in rotated roles); otherwise every value is read from shared
-    // memory and three plane stages are held (fewer registers, one code copy)
-    static constexpr bool CARRY = CARRY_ != 0;
     static constexpr int TY = NCW * RPW;
     static constexpr int CPL = TX / 64;
     static constexpr int HX = 4;      // halo columns kept left of the tile in smem
@@ -167,7 +167,8 @@ struct Tile {
     static constexpr int STAGE_BYTES = (W * H * 8 + 127) / 128 * 128;
     static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8 + 2 * 4 * 8 + 4 * 4 + 128;
     static constexpr int THREADS = 32 * (NCW + 1);
-    static_assert(TX % 64 == 0 && W <= 256 && H <= 256 && NSTAGE >= (CARRY ? 3 : 4), "tile shape");
+    // the consumers hold the stages of planes z-1, z, z+1; at least one more is in flight
+    static_assert(TX % 64 == 0 && W <= 256 && H <= 256 && NSTAGE >= 4, "tile shape");
 };
 
 // Rare path (strategy C prologue, "unpack fused into the update"): overwrite
@@ -352,9 +353,6 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
     }
 
     // ---------------- consumer warps
-    uint64_t store_policy = 0;
-    const bool hint = flags & 2;
-    if (hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(store_policy));
     int s = 0, qs = 0;
     uint32_t ph = 0, qph = 0;
     auto stage = [&](int i) -> double* { return reinterpret_cast<double*>(smem + i * T::STAGE_BYTES); };
@@ -392,35 +390,25 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                 __syncwarp();
             }
         };
-        auto read_centres = [&](const double* st, double2 (&v)[RPW][CPL]) {
-#pragma unroll
-            for (int r = 0; r < RPW; ++r)
-#pragma unroll
-                for (int c = 0; c < CPL; ++c) v[r][c] = *reinterpret_cast<const double2*>(st + sbase + r * W + 64 * c);
-        };
 
-        // One output plane z.  Hot part: no branches but the store
-        // predicates.  Rare part (a tiny sum needing the subnormal-exact
-        // division, or x faces of the fused epilogue): recompute those cells
-        // from the same inputs and store again / store the face values.
-        // st: stage of plane z (+ this thread's offset); CC/ZM/ZP give the
-        // centre values of planes z, z-1, z+1 for cell pair (r, c).
-        auto compute_plane_t = [&](auto mode_tag, int z, uint32_t fm, const double* st, auto&& CC, auto&& ZM,
-                                   auto&& ZP) {
-            // MODE 0: no face work; 1: x faces only (values captured in the hot
-            // loop, stored by the owning lane afterwards); 2: any faces, inline
+        // One output plane z from the stages of planes z-1 (pm), z (pc), z+1
+        // (pp), all at this thread's offset.  MODE 0: no face work; 1: x faces
+        // only (the boundary values are captured in the hot loop and stored by
+        // the owning lane afterwards); 2: any faces, stored inline (fused
+        // epilogue, "pack fused into the update").  WHOLE: every cell of the
+        // tile is inside the block (no store predicates).  The hot loop has no
+        // branch; a sum whose quotient would be subnormal flags the plane for
+        // a rare exact pass (recompute from the same inputs, store again).
+        auto compute_plane = [&](auto mode_tag, auto whole_tag, int z, uint32_t fm, const double* pm,
+                                 const double* pc, const double* pp) {
             constexpr int MODE = decltype(mode_tag)::value;
+            constexpr bool WHOLE = decltype(whole_tag)::value;
             constexpr bool FACES = MODE == 2;
             double* op = obase + (int64_t)(z + 1) * zs;
             double cap0[RPW], cap1[RPW];  // MODE 1: new values of the x = 0 / x = nx-1 cells of each row
             const int xlast = nx - 1 - x0;  // tile-local x of the last cell
             const int clast = xlast >> 6, lane_last = (xlast & 63) >> 1;
             const bool last_is_x = !(xlast & 1);
-            // Fused epilogue ("pack fused into the update"): faces this plane
-            // feeds are stored inline next to the output -- z faces (the whole
-            // plane) and y faces (whole rows) as 16-byte stores where aligned,
-            // x faces (one cell per row) by the owning lane.  Only the
-            // degenerate nz == 1 case (two z faces) uses the rare pass.
             double* zdst = nullptr;
             int64_t zsb = 0;
             double* ymd = nullptr;
@@ -429,19 +417,19 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
             double* xpd = nullptr;
             int64_t xmsa = 0, xpsa = 0;
             uint32_t rare_faces = 0;
-            if (FACES && (fm & 1u)) {
-                const FaceRef F = load_face(&d->epi[0]);
-                xmd = F.p + (int64_t)z * F.sb;
-                xmsa = F.sa;
-            }
-            if (FACES && (fm & 2u)) {
-                const FaceRef F = load_face(&d->epi[1]);
-                xpd = F.p + (int64_t)z * F.sb;
-                xpsa = F.sa;
-            }
-            if (FACES && (fm & ~3u)) {
+            if constexpr (FACES) {
+                if (fm & 1u) {
+                    const FaceRef F = load_face(&d->epi[0]);
+                    xmd = F.p + (int64_t)z * F.sb;
+                    xmsa = F.sa;
+                }
+                if (fm & 2u) {
+                    const FaceRef F = load_face(&d->epi[1]);
+                    xpd = F.p + (int64_t)z * F.sb;
+                    xpsa = F.sa;
+                }
                 if ((fm & 48u) == 48u) {
-                    rare_faces |= 48u;
+                    rare_faces |= 48u;  // nz == 1: two z faces per cell
                 } else if (fm & 48u) {
                     const FaceRef F = load_face(&d->epi[(fm & 16u) ? 4 : 5]);
                     zdst = F.p;
@@ -461,12 +449,15 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
             for (int r = 0; r < RPW; ++r) {
 #pragma unroll
                 for (int c = 0; c < CPL; ++c) {
-                    const double* p = st + r * W + 64 * c;
-                    const double2 cc = CC(r, c);
+                    const int off = r * W + 64 * c;
+                    const double* p = pc + off;
+                    const double2 cc = *reinterpret_cast<const double2*>(p);
                     const double2 ym = *reinterpret_cast<const double2*>(p - W);
                     const double2 yp = *reinterpret_cast<const double2*>(p + W);
-                    const double s0 = sum7(cc.x, p[-1], cc.y, ym.x, yp.x, ZM(r, c).x, ZP(r, c).x);
-                    const double s1 = sum7(cc.y, cc.x, p[2], ym.y, yp.y, ZM(r, c).y, ZP(r, c).y);
+                    const double2 zm = *reinterpret_cast<const double2*>(pm + off);
+                    const double2 zp = *reinterpret_cast<const double2*>(pp + off);
+                    const double s0 = sum7(cc.x, p[-1], cc.y, ym.x, yp.x, zm.x, zp.x);
+                    const double s1 = sum7(cc.y, cc.x, p[2], ym.y, yp.y, zm.y, zp.y);
                     tiny |= (fabs(s0) < kDiv7Tiny) | (fabs(s1) < kDiv7Tiny);
                     const double vx = div7_fast(s0), vy = div7_fast(s1);
                     if constexpr (MODE == 1) {
@@ -475,35 +466,33 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                     }
                     double* o = op + r * pitch + 64 * c;
                     const int x = xl + 64 * c, y = yl + r;
-                    const bool v1 = whole || (y < ny && x + 1 < nx);
-                    const bool v0 = v1 || (y < ny && x < nx);
-                    if (v1) {
-                        if (hint)
-                            asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(o), "d"(vx),
-                                         "d"(vy), "l"(store_policy)
-                                         : "memory");
-                        else
-                            *reinterpret_cast<double2*>(o) = make_double2(vx, vy);
-                    } else if (v0) {
-                        o[0] = vx;
+                    bool v1 = true, v0 = true;
+                    if constexpr (!WHOLE) {
+                        v1 = y < ny && x + 1 < nx;
+                        v0 = y < ny && x < nx;
                     }
-                    if (FACES && xmd && x == 0 && v0) xmd[y * xmsa] = vx;
-                    if (FACES && xpd && v0) {
-                        if (x == nx - 1) xpd[y * xpsa] = vx;
-                        else if (x + 1 == nx - 1) xpd[y * xpsa] = vy;
-                    }
-                    if (FACES && (fm & ~3u)) {
-                        double* fd[3] = {zdst ? zdst + x + (int64_t)y * zsb : nullptr,
-                                         (ymd && y == 0) ? ymd + x : nullptr, (ypd && y == ny - 1) ? ypd + x : nullptr};
+                    if (v1) st_global_v2(o, vx, vy);
+                    else if (v0) o[0] = vx;
+                    if constexpr (FACES) {
+                        if (xmd && x == 0 && v0) xmd[y * xmsa] = vx;
+                        if (xpd && v0) {
+                            if (x == nx - 1) xpd[y * xpsa] = vx;
+                            else if (x + 1 == nx - 1) xpd[y * xpsa] = vy;
+                        }
+                        if (fm & ~3u) {
+                            double* fd[3] = {zdst ? zdst + x + (int64_t)y * zsb : nullptr,
+                                             (ymd && y == 0) ? ymd + x : nullptr,
+                                             (ypd && y == ny - 1) ? ypd + x : nullptr};
 #pragma unroll
-                        for (int k = 0; k < 3; ++k) {
-                            double* q = fd[k];
-                            if (!q) continue;
-                            if (v1 && !(reinterpret_cast<uintptr_t>(q) & 15)) {
-                                *reinterpret_cast<double2*>(q) = make_double2(vx, vy);
-                            } else {
-                                if (v0) q[0] = vx;
-                                if (v1) q[1] = vy;
+                            for (int k = 0; k < 3; ++k) {
+                                double* q = fd[k];
+                                if (!q) continue;
+                                if (v1 && !(reinterpret_cast<uintptr_t>(q) & 15)) {
+                                    st_global_v2(q, vx, vy);
+                                } else {
+                                    if (v0) q[0] = vx;
+                                    if (v1) q[1] = vy;
+                                }
                             }
                         }
                     }
@@ -525,7 +514,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                         if (yl + r < ny) q[(int64_t)(yl + r) * F.sa] = cap1[r];
                 }
             }
-            if (tiny || (FACES && rare_faces)) {
+            if (tiny || rare_faces) {
 #pragma unroll
                 for (int r = 0; r < RPW; ++r) {
 #pragma unroll
@@ -535,12 +524,15 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                         const bool has2 = x + 1 < nx;
                         const bool onb = (rare_faces & 48u) != 0;
                         if (!tiny && !onb) continue;
-                        const double* p = st + r * W + 64 * c;
-                        const double2 cc = CC(r, c);
+                        const int off = r * W + 64 * c;
+                        const double* p = pc + off;
+                        const double2 cc = *reinterpret_cast<const double2*>(p);
                         const double2 ym = *reinterpret_cast<const double2*>(p - W);
                         const double2 yp = *reinterpret_cast<const double2*>(p + W);
-                        const double vx = div7(sum7(cc.x, p[-1], cc.y, ym.x, yp.x, ZM(r, c).x, ZP(r, c).x));
-                        const double vy = div7(sum7(cc.y, cc.x, p[2], ym.y, yp.y, ZM(r, c).y, ZP(r, c).y));
+                        const double2 zm = *reinterpret_cast<const double2*>(pm + off);
+                        const double2 zp = *reinterpret_cast<const double2*>(pp + off);
+                        const double vx = div7(sum7(cc.x, p[-1], cc.y, ym.x, yp.x, zm.x, zp.x));
+                        const double vy = div7(sum7(cc.y, cc.x, p[2], ym.y, yp.y, zm.y, zp.y));
                         double* o = op + r * pitch + 64 * c;
                         o[0] = vx;
                         if (has2) o[1] = vy;
@@ -551,77 +543,39 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                 }
             }
         };
-        // planes without face work (the vast majority) run a loop with no
-        // epilogue code at all
-        auto compute_plane = [&](int z, const double* st, auto&& CC, auto&& ZM, auto&& ZP) {
-            const uint32_t fm = epi & (touch | (z == 0 ? 16u : 0u) | (z == nz - 1 ? 32u : 0u));
-            if (fm & ~3u) compute_plane_t(std::integral_constant<int, 2>{}, z, fm, st, CC, ZM, ZP);
-            else if (fm) compute_plane_t(std::integral_constant<int, 1>{}, z, fm, st, CC, ZM, ZP);
-            else compute_plane_t(std::integral_constant<int, 0>{}, z, 0u, st, CC, ZM, ZP);
-        };
 
-        int scur;
-        if constexpr (T::CARRY) {
-            double2 A[RPW][CPL], B[RPW][CPL], C[RPW][CPL];
-            acquire(w.z0 - 1);
-            read_centres(stage(s), A);
+        // stages of planes z-1, z, z+1 are held; every value is read from smem
+        acquire(w.z0 - 1);
+        int sm = s;
+        advance();
+        acquire(w.z0);
+        int sc = s;
+        advance();
+        for (int z = w.z0; z < w.z1; ++z) {
+            acquire(z + 1);
+            const int sp = s;
+            advance();
+            const double* pm = stage(sm) + sbase;
+            const double* pc = stage(sc) + sbase;
+            const double* pp = stage(sp) + sbase;
+            const uint32_t fm = epi & (touch | (z == 0 ? 16u : 0u) | (z == nz - 1 ? 32u : 0u));
+            using M0 = std::integral_constant<int, 0>;
+            using M1 = std::integral_constant<int, 1>;
+            using M2 = std::integral_constant<int, 2>;
+            if (fm & ~3u) compute_plane(M2{}, std::false_type{}, z, fm, pm, pc, pp);
+            else if (fm) compute_plane(M1{}, std::false_type{}, z, fm, pm, pc, pp);
+            else if (whole) compute_plane(M0{}, std::true_type{}, z, 0u, pm, pc, pp);
+            else compute_plane(M0{}, std::false_type{}, z, 0u, pm, pc, pp);
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
-            advance();
-            acquire(w.z0);
-            read_centres(stage(s), B);
-            scur = s;
-            advance();
-            // (P = z-1, Q = z, N <- z+1) in rotated roles: no register moves
-            auto plane = [&](int z, const double2 (&P)[RPW][CPL], const double2 (&Q)[RPW][CPL],
-                             double2 (&N)[RPW][CPL]) {
-                acquire(z + 1);
-                read_centres(stage(s), N);
-                compute_plane(
-                    z, stage(scur) + sbase, [&](int r, int c) { return Q[r][c]; },
-                    [&](int r, int c) { return P[r][c]; }, [&](int r, int c) { return N[r][c]; });
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[scur]);
-                scur = s;
-                advance();
-            };
-            for (int z = w.z0;;) {
-                if (z >= w.z1) break;
-                plane(z++, A, B, C);
-                if (z >= w.z1) break;
-                plane(z++, B, C, A);
-                if (z >= w.z1) break;
-                plane(z++, C, A, B);
-            }
-        } else {
-            // stages of planes z-1, z, z+1 are held; everything read from smem
-            acquire(w.z0 - 1);
-            int sm = s;
-            advance();
-            acquire(w.z0);
-            scur = s;
-            advance();
-            for (int z = w.z0; z < w.z1; ++z) {
-                acquire(z + 1);
-                const int sp = s;
-                advance();
-                const double* pm = stage(sm) + sbase;
-                const double* pc = stage(scur) + sbase;
-                const double* pp = stage(sp) + sbase;
-                compute_plane(
-                    z, pc, [&](int r, int c) { return *reinterpret_cast<const double2*>(pc + r * W + 64 * c); },
-                    [&](int r, int c) { return *reinterpret_cast<const double2*>(pm + r * W + 64 * c); },
-                    [&](int r, int c) { return *reinterpret_cast<const double2*>(pp + r * W + 64 * c); });
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[sm]);
-                sm = scur;
-                scur = sp;
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[sm]);  // plane z1-1
+            if (lane == 0) mbar_arrive(&empty[sm]);
+            sm = sc;
+            sc = sp;
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[scur]);  // plane z1
+        if (lane == 0) {
+            mbar_arrive(&empty[sm]);  // plane z1-1
+            mbar_arrive(&empty[sc]);  // plane z1
+        }
     }
 }
 
@@ -750,29 +704,16 @@ cudaError_t launch_div7_selftest(uint64_t n, uint64_t seed, unsigned long long* 
 // ------------------------------------------------------------------ host launchers
 // Tile configurations selectable at run time (kind index):
 //          TX  NCW RPW NSTAGE MINB      tile     CTAs/SM (smem)
-#define J3D_TILES(X)                                                             \
-    X(0, 128, 8, 2, 4, 2, 1)    /* 128x16, 4 x 19 KB stages                    */ \
-    X(1, 64, 8, 2, 4, 2, 1)     /* 64x16, 4 x 9.8 KB                           */ \
-    X(2, 64, 8, 2, 6, 2, 1)     /* 64x16, 6 stages                             */ \
-    X(3, 128, 8, 2, 8, 1, 1)    /* 128x16, 8 stages, 1 CTA/SM                  */ \
-    X(4, 128, 8, 1, 6, 2, 1)    /* 128x8, 6 x 10.5 KB                          */ \
-    X(5, 64, 16, 2, 6, 1, 1)    /* 64x32, 16 consumer warps                    */ \
-    X(6, 64, 16, 1, 6, 2, 1)    /* 64x16, 16 consumer warps                    */ \
-    X(7, 64, 8, 1, 6, 3, 1)     /* 64x8, 3 CTAs/SM                             */ \
-    X(8, 64, 8, 2, 4, 3, 1)     /* 64x16, 3 CTAs/SM                            */ \
-    X(9, 128, 16, 1, 4, 1, 1)   /* 128x16, 16 consumer warps, 1 CTA/SM         */ \
-    X(10, 128, 8, 1, 8, 2, 1)   /* 128x8, 8 stages                             */ \
-    X(11, 128, 15, 2, 4, 1, 1)  /* 128x30, 15 consumer warps, 4 x 34 KB        */ \
-    X(12, 128, 11, 2, 6, 1, 1)  /* 128x22, 11 consumer warps, 6 x 25 KB        */ \
-    X(13, 128, 15, 2, 6, 1, 0)  /* 128x30 from smem only, 6 x 34 KB            */ \
-    X(14, 128, 8, 2, 5, 2, 0)   /* 128x16 from smem only, 5 x 19 KB, 2 CTA/SM  */ \
-    X(15, 64, 8, 2, 6, 2, 0)    /* 64x16 from smem only                        */ \
-    X(16, 128, 15, 2, 5, 1, 0)  /* 128x30 from smem only, 5 stages             */ \
-    X(17, 64, 8, 2, 7, 3, 0)    /* 64x16 from smem only, 3 CTAs/SM             */ \
-    X(18, 128, 8, 1, 8, 2, 0)   /* 128x8 from smem only, 8 stages              */ \
-    X(19, 192, 11, 2, 5, 1, 0)  /* 192x22 from smem only, 5 x 37.6 KB          */ \
-    X(20, 192, 15, 2, 4, 1, 0)  /* 192x30 from smem only, 4 x 50 KB            */ \
-    X(21, 128, 12, 2, 5, 1, 0)  /* 128x24 from smem only (96-wide blocks)     */
+#define J3D_TILES(X)                                                    \
+    X(0, 192, 11, 2, 5, 1)  /* 192x22, 5 x 38 KB stages, 1 CTA/SM       */ \
+    X(1, 128, 15, 2, 5, 1)  /* 128x30, 5 x 35 KB, 1 CTA/SM               */ \
+    X(2, 64, 8, 2, 7, 3)    /* 64x16, 7 x 10 KB, 3 CTAs/SM               */ \
+    X(3, 128, 8, 2, 5, 2)   /* 128x16, 5 x 20 KB, 2 CTAs/SM              */ \
+    X(4, 64, 8, 2, 6, 2)    /* 64x16, 6 stages, 2 CTAs/SM                */ \
+    X(5, 128, 8, 1, 8, 2)   /* 128x8, 8 stages, 2 CTAs/SM                */ \
+    X(6, 192, 15, 2, 4, 1)  /* 192x30, 4 x 51 KB                         */ \
+    X(7, 128, 12, 2, 5, 1)  /* 128x24                                    */ \
+    X(8, 128, 15, 2, 6, 1)  /* 128x30, 6 stages                          */
 
 template <class T>
 static cudaError_t launch_t(const StencilLaunch& L, cudaStream_t st) {
@@ -798,13 +739,13 @@ static cudaError_t occ_t(int* blocks) {
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, stencil_tma_kernel<T>, T::THREADS, T::SMEM_BYTES);
 }
 
-#define J3D_TYPE(k, tx, ncw, rpw, ns, mb, cy) Tile<tx, ncw, rpw, ns, mb, cy>
+#define J3D_TYPE(k, tx, ncw, rpw, ns, mb) Tile<tx, ncw, rpw, ns, mb>
 
-int num_tile_kinds() { return 22; }
+int num_tile_kinds() { return 9; }
 
 TileShape tile_shape(int kind) {
     switch (kind) {
-#define X(k, tx, ncw, rpw, ns, mb, cy) \
+#define X(k, tx, ncw, rpw, ns, mb) \
     case k: return TileShape{tx, ncw * rpw};
         J3D_TILES(X)
 #undef X
@@ -814,8 +755,8 @@ TileShape tile_shape(int kind) {
 
 cudaError_t launch_stencil(const StencilLaunch& L, cudaStream_t st) {
     switch (L.kind) {
-#define X(k, tx, ncw, rpw, ns, mb, cy) \
-    case k: return launch_t<J3D_TYPE(k, tx, ncw, rpw, ns, mb, cy)>(L, st);
+#define X(k, tx, ncw, rpw, ns, mb) \
+    case k: return launch_t<J3D_TYPE(k, tx, ncw, rpw, ns, mb)>(L, st);
         J3D_TILES(X)
 #undef X
     }
@@ -824,8 +765,8 @@ cudaError_t launch_stencil(const StencilLaunch& L, cudaStream_t st) {
 
 cudaError_t stencil_occupancy(int kind, bool, int* blocks_per_sm) {
     switch (kind) {
-#define X(k, tx, ncw, rpw, ns, mb, cy) \
-    case k: return occ_t<J3D_TYPE(k, tx, ncw, rpw, ns, mb, cy)>(blocks_per_sm);
+#define X(k, tx, ncw, rpw, ns, mb) \
+    case k: return occ_t<J3D_TYPE(k, tx, ncw, rpw, ns, mb)>(blocks_per_sm);
         J3D_TILES(X)
 #undef X
     }
