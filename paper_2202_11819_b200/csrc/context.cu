@@ -27,6 +27,8 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <array>
 #include <cstdio>
 #include <cstdlib>
@@ -1078,11 +1080,43 @@ void destroy_ctx(jacobi3d* c) {
     delete c;
 }
 
+// Host wait for all work queued on `st`.  Multi-GPU contexts poll with a
+// watchdog (J3D_TIMEOUT_S, default 600 s): a peer that never signals its
+// epoch (or an NCCL error) surfaces as J3D_ETIMEOUT / J3D_ENCCL instead of a
+// hang.
+void wait_stream(jacobi3d* c, cudaStream_t st) {
+    if (c->n_gpus == 1) {
+        CK(cudaStreamSynchronize(st));
+        return;
+    }
+    double limit = 600.0;
+    if (const char* e = std::getenv("J3D_TIMEOUT_S")) limit = std::atof(e);
+    const auto t0 = std::chrono::steady_clock::now();
+    int us = 20;
+    for (;;) {
+        const cudaError_t q = cudaStreamQuery(st);
+        if (q == cudaSuccess) return;
+        if (q != cudaErrorNotReady) CK(q);
+        if (c->comm) {
+            ncclResult_t ar = ncclSuccess;
+            NK(ncclCommGetAsyncError(c->comm, &ar));
+            NK(ar);
+        }
+        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (el > limit)
+            throw Error(J3D_ETIMEOUT, "cross-GPU wait did not complete within " + std::to_string((int)limit) +
+                                          " s (a peer rank stopped, or the ranks called the collective API in "
+                                          "different orders)");
+        std::this_thread::sleep_for(std::chrono::microseconds(us));
+        us = std::min(us * 2, 2000);
+    }
+}
+
 void nccl_barrier(jacobi3d* c) {
     if (c->n_gpus == 1 || !c->comm) return;
     double* s = (double*)(c->arena + c->off_scratch + 64);
     NK(ncclAllReduce(s, s, 1, ncclFloat64, ncclSum, c->comm, c->main));
-    CK(cudaStreamSynchronize(c->main));
+    wait_stream(c, c->main);
 }
 
 }  // namespace
@@ -1367,7 +1401,7 @@ int jacobi3d_set_block(jacobi3d_t* c, int64_t id, const double* host_in) {
         CK(cudaSetDevice(c->device));
         cudaMemcpy3DParms m = owned_copy(c, l, (int)(c->iter & 1), const_cast<double*>(host_in), false);
         CK(cudaMemcpy3DAsync(&m, c->main));
-        CK(cudaStreamSynchronize(c->main));
+        wait_stream(c, c->main);
         c->halos_stale = true;
         c->iter_since_set = 0;
         return J3D_OK;
@@ -1383,7 +1417,7 @@ int jacobi3d_get_block(jacobi3d_t* c, int64_t id, double* host_out) {
         CK(cudaSetDevice(c->device));
         cudaMemcpy3DParms m = owned_copy(c, l, (int)(c->iter & 1), host_out, true);
         CK(cudaMemcpy3DAsync(&m, c->main));
-        CK(cudaStreamSynchronize(c->main));
+        wait_stream(c, c->main);
         return J3D_OK;
     });
 }
@@ -1406,7 +1440,7 @@ int jacobi3d_get_region(jacobi3d_t* c, int64_t id, const int64_t lo[3], const in
         m.kind = cudaMemcpyDeviceToHost;
         m.extent = make_cudaExtent((size_t)ext[0] * 8, (size_t)ext[1], (size_t)ext[2]);
         CK(cudaMemcpy3DAsync(&m, c->main));
-        CK(cudaStreamSynchronize(c->main));
+        wait_stream(c, c->main);
         return J3D_OK;
     });
 }
@@ -1439,7 +1473,7 @@ int jacobi3d_synchronize(jacobi3d_t* c) {
     return guarded([&]() -> int {
         if (!c) return fail(J3D_EINVAL, "ctx is NULL");
         CK(cudaSetDevice(c->device));
-        CK(cudaStreamSynchronize(c->main));
+        wait_stream(c, c->main);
         CK(cudaDeviceSynchronize());
         if (c->comm) {
             ncclResult_t ar = ncclSuccess;
@@ -1462,7 +1496,7 @@ int jacobi3d_residual(jacobi3d_t* c, double* out) {
         if (c->n_gpus > 1) NK(ncclAllReduce(acc, acc, 1, ncclUint64, ncclMax, c->comm, c->main));
         unsigned long long h = 0;
         CK(cudaMemcpyAsync(&h, acc, 8, cudaMemcpyDeviceToHost, c->main));
-        CK(cudaStreamSynchronize(c->main));
+        wait_stream(c, c->main);
         double d;
         std::memcpy(&d, &h, 8);
         *out = d;
@@ -1481,7 +1515,7 @@ int jacobi3d_checksum(jacobi3d_t* c, uint64_t* out) {
         if (c->n_gpus > 1) NK(ncclAllReduce(acc, acc, 1, ncclUint64, ncclSum, c->comm, c->main));
         unsigned long long h = 0;
         CK(cudaMemcpyAsync(&h, acc, 8, cudaMemcpyDeviceToHost, c->main));
-        CK(cudaStreamSynchronize(c->main));
+        wait_stream(c, c->main);
         *out = (uint64_t)h;
         return J3D_OK;
     });
@@ -1492,11 +1526,13 @@ int jacobi3d_time(jacobi3d_t* c, int64_t warmup, int64_t iters, double* ms) {
         if (!c || !ms || iters < 1 || warmup < 0) return fail(J3D_EINVAL, "bad argument");
         CK(cudaSetDevice(c->device));
         do_iterate(c, warmup);
+        wait_stream(c, c->main);
         CK(cudaDeviceSynchronize());
         nccl_barrier(c);
         CK(cudaEventRecord(c->ev_t0, c->main));
         do_iterate(c, iters);
         CK(cudaEventRecord(c->ev_t1, c->main));
+        wait_stream(c, c->main);
         CK(cudaEventSynchronize(c->ev_t1));
         float f = 0;
         CK(cudaEventElapsedTime(&f, c->ev_t0, c->ev_t1));
