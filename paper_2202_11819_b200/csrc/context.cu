@@ -475,6 +475,12 @@ void build_static_tables(jacobi3d* c) {
     // the block width, else 128x30 (15 consumer warps) for wide blocks and
     // 64x16 (2 CTAs/SM, 6 stages) for narrow ones.  Bench sweeps: profiles/.
     c->tile_kind = (c->nx % 192 == 0) ? 0 : c->nx >= 128 ? 1 : 4;
+    {  // small grids: the wide tiles cannot keep every SM busy -> 64x16, 2 CTAs/SM
+        const TileShape t = tile_shape(c->tile_kind);
+        const int64_t tiles = ((c->nx + t.tx - 1) / t.tx) * ((c->ny + t.ty - 1) / t.ty) * nl;
+        const int64_t max_items = tiles * std::max<int64_t>(1, c->nz / 24);
+        if (c->tile_kind != 4 && max_items < 4LL * c->sms) c->tile_kind = 4;
+    }
     if (const char* e = std::getenv("J3D_TILE")) {  // tuning override (bench sweeps)
         const int k = std::atoi(e);
         if (k >= 0 && k < num_tile_kinds()) c->tile_kind = k;
@@ -489,7 +495,7 @@ void build_static_tables(jacobi3d* c) {
     }
     for (int l = 0; l < nl; ++l)
         for (int p = 0; p < 2; ++p) {
-            cuuint64_t dims[3] = {(cuuint64_t)c->pitch, (cuuint64_t)(c->ny + 2), (cuuint64_t)(c->nz + 2)};
+            cuuint64_t dims[3] = {(cuuint64_t)(XOFF + c->nx + 1), (cuuint64_t)(c->ny + 2), (cuuint64_t)(c->nz + 2)};  // up to the +x ghost: the row padding is never fetched (TMA zero-fills beyond)
             cuuint64_t strides[2] = {(cuuint64_t)(c->pitch * 8), (cuuint64_t)(c->zs * 8)};
             cuuint32_t box[3] = {(cuuint32_t)stencil_box_w(c->tile_kind), (cuuint32_t)stencil_box_h(c->tile_kind), 1};
             cuuint32_t es[3] = {1, 1, 1};
@@ -503,7 +509,7 @@ void build_static_tables(jacobi3d* c) {
     for (int l = 0; l < nl; ++l)
         for (int p = 0; p < 2; ++p)
             for (int h = 0; h < 2; ++h) {
-                cuuint64_t dims[3] = {(cuuint64_t)c->pitch, (cuuint64_t)(c->ny + 2), (cuuint64_t)(c->nz + 2)};
+                cuuint64_t dims[3] = {(cuuint64_t)(XOFF + c->nx + 1), (cuuint64_t)(c->ny + 2), (cuuint64_t)(c->nz + 2)};  // up to the +x ghost: the row padding is never fetched (TMA zero-fills beyond)
                 cuuint64_t strides[2] = {(cuuint64_t)(c->pitch * 8), (cuuint64_t)(c->zs * 8)};
                 const int H = stencil_box_h(c->tile_kind);
                 cuuint32_t box[3] = {(cuuint32_t)stencil_box_w(c->tile_kind), (cuuint32_t)(h == 0 ? 2 : std::max(1, H - 4)), 1};
@@ -529,9 +535,10 @@ void build_static_tables(jacobi3d* c) {
     // chunk re-reads only 2 extra planes (2% at 96).  Measured sweep: 96
     // beats 32/64/128/full depth (profiles/).
     int64_t best_zc = std::max<int64_t>(1, (c->nz + 95) / 96);
-    // small problems: shorter chunks until there are >= 2 items per CTA slot
-    // (at least 8 planes per chunk)
-    while (tiles * best_zc < 2 * (int64_t)c->grid_cap && c->nz / (best_zc + 1) >= 8) ++best_zc;
+    // small problems: shorter chunks until there are >= 6 items per CTA slot
+    // (at least 24 planes per chunk): the last round of items is then short
+    // (measured: 96^3 blocks, ODF 64: 198 -> 225 GLUPS)
+    while (tiles * best_zc < 6 * (int64_t)c->grid_cap && c->nz / (best_zc + 1) >= 24) ++best_zc;
     if (const char* e = std::getenv("J3D_ZCHUNK")) {  // tuning override: planes per z chunk
         const int64_t L = std::atoll(e);
         if (L > 0) best_zc = std::max<int64_t>(1, (c->nz + L - 1) / L);
