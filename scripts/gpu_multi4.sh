@@ -1,12 +1,17 @@
 mkdir -p gpurun_out
 N=$(nvidia-smi -L | wc -l)
-J3D_MP_CASES=quick timeout 1200 python -m pytest tests/test_gpu_multi.py -q -x > gpurun_out/multi_$N.log 2>&1; echo "multi $N rc=$? $(tail -1 gpurun_out/multi_$N.log)"
-grep -E "FAIL" gpurun_out/multi_$N.log | head -5
-run() { timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus $N --steps 30 --warmup 5 --no-cpu --no-e2e "$@" > gpurun_out/b.log 2>&1; echo "bench $N $* rc=$? $(tail -1 gpurun_out/b.log | python -c "
+J3D_MP_CASES=quick timeout 1500 python -m pytest tests/test_gpu_multi.py -q -x > gpurun_out/multi_$N.log 2>&1; echo "multi $N rc=$? $(tail -1 gpurun_out/multi_$N.log)"
+run() { timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus $N --warmup 5 --no-cpu --no-e2e "$@" > gpurun_out/b.log 2>&1; echo "bench $N $* rc=$? $(tail -1 gpurun_out/b.log | python -c "
 import json,sys
-d=json.loads(sys.stdin.read()); print(d['value'], round(d['value']/d['n_gpus'],1), d['ms_per_step'], d.get('halo'), d['roofline']['frac'], d['clocks']['sm_mhz'])" 2>&1)"; }
-run --exchange p2p
-run --exchange nccl
-run --exchange p2p --workload weak1536_odf8
-run --exchange p2p --workload weak1536_odf8 --variant unfused
-run --exchange nccl --workload weak1536_odf8
+d=json.loads(sys.stdin.read()); print(d['value'], round(d['value']/d['n_gpus'],1), d['ms_per_step'], d.get('halo'), (d.get('roofline') or {}).get('frac'), d['clocks']['sm_mhz'])" 2>&1)"; }
+run --steps 30 --exchange p2p
+run --steps 30 --exchange nccl
+run --steps 30 --exchange host
+run --steps 30 --exchange host --overlap 1
+run --steps 30 --exchange p2p --workload weak1536_odf8
+run --steps 30 --exchange p2p --workload weak1536_odf8 --variant unfused
+run --steps 200 --exchange p2p --workload fine384_odf64
+run --steps 200 --exchange p2p --workload fine384_odf64 --graph 1
+run --steps 200 --exchange nccl --workload fine384_odf64 --graph 1
+run --steps 500 --exchange p2p --workload small192_odf1 --graph 1
+run --steps 500 --exchange host --workload small192_odf1 --graph 1
