@@ -164,6 +164,7 @@ struct jacobi3d {
     BlockGeom* d_geom = nullptr;
     unsigned int* d_sched = nullptr;            // [2*(n_local+1)] stencil work counters
     bool store_hint = false;
+    bool xsector_ok = true;  // J3D_XSECTOR=0 disables whole-sector x-ghost stores (tuning)
     std::vector<int> item_begin, item_count;  // per local block, in d_items
     std::vector<int64_t> item_cells;          // prefix sums of owned cells per item (profiling bytes)
     int n_items = 0, tile_kind = 0, grid_cap = 0;
@@ -382,6 +383,7 @@ void build_tables(jacobi3d* c) {
                         if (k == PEER_P2P && !c->p2p_connected) continue;  // filled after ipc_connect
                         d.epi[f] = c->layer(c->buf(c->nbr_local[l][f], q, r), f ^ 1, true);
                         d.epi_mask |= 1u << f;
+                        if (f < 2 && (c->nx % 4) == 0 && c->xsector_ok) d.xsector |= 1u << f;  // whole-sector x-ghost stores
                     } else if (v == J3D_FUSE_DIRECT) {
                         // NCCL face of the direct variant: epilogue packs into the
                         // send buffer; after the exchange a batched unpack kernel
@@ -1229,6 +1231,7 @@ int jacobi3d_create(const jacobi3d_config* cfg, const uint8_t* nccl_uid, jacobi3
         CK(cudaMalloc(&c->d_sched, sizeof(unsigned int) * 2 * (c->n_local + 1)));
         CK(cudaMemset(c->d_sched, 0, sizeof(unsigned int) * 2 * (c->n_local + 1)));
         if (const char* e = std::getenv("J3D_STORE_HINT")) c->store_hint = std::atoi(e) != 0;
+        if (const char* e = std::getenv("J3D_XSECTOR")) c->xsector_ok = std::atoi(e) != 0;
         c->peer_base.assign(c->n_gpus, nullptr);
         build_static_tables(c);
         build_tables(c);

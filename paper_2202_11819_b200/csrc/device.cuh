@@ -30,7 +30,9 @@ struct StencilDesc {
     uint32_t epi_mask;  // faces whose new boundary layer the epilogue stores to epi[f]
     int64_t pitch, zs;
     uint32_t pro_mask;  // faces whose ghost values the prologue reads from pro[f]
-    uint32_t pad;
+    uint32_t xsector;   // bit f (f = 0, 1): epi[f] is an x ghost column of a buffer (layout above);
+                        // the epilogue may then write its whole 32-byte sector (ghost + 3 padding
+                        // columns) so no partial-sector read-modify-write reaches HBM
     FaceRef epi[6];
     FaceRef pro[6];
 };

@@ -99,6 +99,21 @@ __device__ __forceinline__ void st_global_v2(double* p, double a, double b) {
     asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
 }
 
+// Store one x-ghost value as its whole 32-byte sector.  q points at the ghost
+// cell; `left`: the ghost is the -x ghost (column XOFF-1, the last double of
+// its sector: columns XOFF-4..XOFF-2 are padding) else the +x ghost (column
+// XOFF+nx, first of its sector, nx % 4 == 0: the rest is row padding).
+__device__ __forceinline__ void st_ghost_sector(double* q, double v, bool left) {
+    double* b = left ? q - 3 : q;
+    if (left) {
+        st_global_v2(b, 0.0, 0.0);
+        st_global_v2(b + 2, 0.0, v);
+    } else {
+        st_global_v2(b, v, 0.0);
+        st_global_v2(b + 2, 0.0, 0.0);
+    }
+}
+
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     uint64_t z = x + 0x9E3779B97F4A7C15ULL;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -379,6 +394,16 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
         const uint32_t touch = (x0 == 0 ? 1u : 0u) | (x0 + T::TX >= nx ? 2u : 0u) | (y0 == 0 ? 4u : 0u) |
                                (y0 + T::TY >= ny ? 8u : 0u);
         const bool whole = x0 + T::TX <= nx && y0 + T::TY <= ny;  // no cell of the tile is outside the block
+        // x-face destinations of this tile: wide tiles load them once per item
+        // (registers are plentiful there), narrow 2-CTA/SM tiles per plane
+        constexpr bool HOISTX = T::TX >= 128;
+        FaceRef fxm{nullptr, 0, 0}, fxp{nullptr, 0, 0};
+        if (HOISTX && (epi & touch & 1u)) fxm = load_face(&d->epi[0]);
+        if (HOISTX && (epi & touch & 2u)) fxp = load_face(&d->epi[1]);
+        auto face_x = [&](int f) -> FaceRef {
+            if constexpr (HOISTX) return f == 0 ? fxm : fxp;
+            else return load_face(&d->epi[f]);
+        };
         const int sbase = (warp * RPW + 1) * W + 2 * lane + T::HX;  // smem offset of cell (r = 0, c = 0)
 
         // wait for the stage of plane zz, patch its ghosts (fused prologue) if needed
@@ -419,12 +444,12 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
             uint32_t rare_faces = 0;
             if constexpr (FACES) {
                 if (fm & 1u) {
-                    const FaceRef F = load_face(&d->epi[0]);
+                    const FaceRef F = face_x(0);
                     xmd = F.p + (int64_t)z * F.sb;
                     xmsa = F.sa;
                 }
                 if (fm & 2u) {
-                    const FaceRef F = load_face(&d->epi[1]);
+                    const FaceRef F = face_x(1);
                     xpd = F.p + (int64_t)z * F.sb;
                     xpsa = F.sa;
                 }
@@ -474,10 +499,18 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                     if (v1) st_global_v2(o, vx, vy);
                     else if (v0) o[0] = vx;
                     if constexpr (FACES) {
-                        if (xmd && x == 0 && v0) xmd[y * xmsa] = vx;
+                        if (xmd && x == 0 && v0) {
+                            // my -x face feeds the neighbour's +x ghost
+                            if (d->xsector & 1u) st_ghost_sector(xmd + y * xmsa, vx, false);
+                            else xmd[y * xmsa] = vx;
+                        }
                         if (xpd && v0) {
-                            if (x == nx - 1) xpd[y * xpsa] = vx;
-                            else if (x + 1 == nx - 1) xpd[y * xpsa] = vy;
+                            const bool hit0 = x == nx - 1, hit1 = x + 1 == nx - 1;
+                            if (hit0 || hit1) {
+                                const double v = hit0 ? vx : vy;
+                                if (d->xsector & 2u) st_ghost_sector(xpd + y * xpsa, v, true);
+                                else xpd[y * xpsa] = v;
+                            }
                         }
                         if (fm & ~3u) {
                             double* fd[3] = {zdst ? zdst + x + (int64_t)y * zsb : nullptr,
@@ -500,18 +533,24 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
             }
             if constexpr (MODE == 1) {
                 if ((fm & 1u) && x0 == 0 && lane == 0) {
-                    const FaceRef F = load_face(&d->epi[0]);
+                    const FaceRef F = face_x(0);
                     double* q = F.p + (int64_t)z * F.sb;
 #pragma unroll
                     for (int r = 0; r < RPW; ++r)
-                        if (yl + r < ny) q[(int64_t)(yl + r) * F.sa] = cap0[r];
+                        if (yl + r < ny) {
+                            if (d->xsector & 1u) st_ghost_sector(q + (int64_t)(yl + r) * F.sa, cap0[r], false);
+                            else q[(int64_t)(yl + r) * F.sa] = cap0[r];
+                        }
                 }
                 if ((fm & 2u) && clast < CPL && lane == lane_last) {
-                    const FaceRef F = load_face(&d->epi[1]);
+                    const FaceRef F = face_x(1);
                     double* q = F.p + (int64_t)z * F.sb;
 #pragma unroll
                     for (int r = 0; r < RPW; ++r)
-                        if (yl + r < ny) q[(int64_t)(yl + r) * F.sa] = cap1[r];
+                        if (yl + r < ny) {
+                            if (d->xsector & 2u) st_ghost_sector(q + (int64_t)(yl + r) * F.sa, cap1[r], true);
+                            else q[(int64_t)(yl + r) * F.sa] = cap1[r];
+                        }
                 }
             }
             if (tiny || rare_faces) {
@@ -713,7 +752,10 @@ cudaError_t launch_div7_selftest(uint64_t n, uint64_t seed, unsigned long long* 
     X(5, 128, 8, 1, 8, 2)   /* 128x8, 8 stages, 2 CTAs/SM                */ \
     X(6, 192, 15, 2, 4, 1)  /* 192x30, 4 x 51 KB                         */ \
     X(7, 128, 12, 2, 5, 1)  /* 128x24                                    */ \
-    X(8, 128, 15, 2, 6, 1)  /* 128x30, 6 stages                          */
+    X(8, 128, 15, 2, 6, 1)  /* 128x30, 6 stages                          */ \
+    X(9, 64, 6, 2, 6, 2)    /* 64x12, 2 CTAs/SM (7 warps)                */ \
+    X(10, 64, 12, 2, 6, 1)  /* 64x24, 1 CTA/SM                           */ \
+    X(11, 64, 7, 2, 6, 2)   /* 64x14, 2 CTAs/SM (8 warps)                */
 
 template <class T>
 static cudaError_t launch_t(const StencilLaunch& L, cudaStream_t st) {
@@ -741,7 +783,7 @@ static cudaError_t occ_t(int* blocks) {
 
 #define J3D_TYPE(k, tx, ncw, rpw, ns, mb) Tile<tx, ncw, rpw, ns, mb>
 
-int num_tile_kinds() { return 9; }
+int num_tile_kinds() { return 12; }
 
 TileShape tile_shape(int kind) {
     switch (kind) {
