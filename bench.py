@@ -273,7 +273,7 @@ def main():
                 "ms_per_iter_exchange_elided": round(float(t2.item()), 4)}
 
     cpu = None
-    if rank == 0 and not a.no_cpu:
+    if rank == 0 and world == 1 and not a.no_cpu:  # the oracle baseline: rank 0 at N=1 only
         cpu = cpu_baseline(grid)
 
     ctx.close()

@@ -97,6 +97,33 @@ def run_fullsize(world):
     return checked
 
 
+def run_set_block_case(grid, odf, variant, exchange):
+    """Host upload on every rank (jacobi3d_set_block), collective refresh, run;
+    iterate before the refresh must fail with J3D_ESTATE on multi-GPU."""
+    from inputs.generators import uniform_field
+    import paper_2202_11819_b200 as j3d
+
+    U0 = uniform_field(*grid, seed=17, boundary=0.25)
+    ctx = jdist.create(grid, odf=odf, variant=variant, exchange=exchange, boundary=0.25)
+    try:
+        ctx.init("default")
+        ctx.scatter_local(U0[1:-1, 1:-1, 1:-1])
+        try:
+            ctx.iterate(1)
+            raise AssertionError("iterate with stale halos must fail on a multi-GPU context")
+        except j3d.Jacobi3DError as e:
+            assert e.code == j3d.jacobi3d.ESTATE, e
+        ctx.refresh_halos()
+        ctx.iterate(6)
+        got = ctx.gather_local()
+        want = core.owned(core.run(U0, 6))
+        mask = ~np.isnan(got)
+        assert (got.view(np.uint64)[mask] == np.ascontiguousarray(want).view(np.uint64)[mask]).all(), \
+            f"set_block case {variant}/{exchange}"
+    finally:
+        ctx.close()
+
+
 def main():
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
@@ -140,6 +167,14 @@ def main():
         cases += [((16, 8, 16), 1, v, "batched", False, "p2p", 2, "hash", 3) for v in ("unfused", "C")]
         cases += [((16, 8, 16), 1, v, "batched", False, "host", 2, "hash", 3) for v in ("unfused", "direct")]
     n, failed = 0, []
+    if which != "debug":
+        for v, x in (("direct", "p2p"), ("unfused", "nccl"), ("C", "host")):
+            try:
+                run_set_block_case(g, 2, v, x)
+            except AssertionError as e:
+                failed.append(str(e))
+                print("FAIL", e, flush=True)
+            n += 1
     for c in cases:
         try:
             run_case(*c)
