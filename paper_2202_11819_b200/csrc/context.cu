@@ -163,7 +163,6 @@ struct jacobi3d {
     bool direct_nccl_unpack = false;
     BlockGeom* d_geom = nullptr;
     unsigned int* d_sched = nullptr;            // [2*(n_local+1)] stencil work counters
-    bool store_hint = false;
     bool xsector_ok = true;  // J3D_XSECTOR=0 disables whole-sector x-ghost stores (tuning)
     std::vector<int> item_begin, item_count;  // per local block, in d_items
     std::vector<int64_t> item_cells;          // prefix sums of owned cells per item (profiling bytes)
@@ -648,7 +647,6 @@ void stencil(jacobi3d* c, int begin, int count, int parity, cudaStream_t st, int
     L.grid = std::min(count, c->grid_cap);
     L.kind = c->tile_kind;
     L.faces = c->faces_fused;
-    L.store_hint = c->store_hint;
     L.sched = c->d_sched + 2 * (l + 1);  // one counter pair per concurrently running launch
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     const bool prof = c->prof && !c->capturing;
@@ -1230,7 +1228,6 @@ int jacobi3d_create(const jacobi3d_config* cfg, const uint8_t* nccl_uid, jacobi3
         CK(cudaMalloc(&c->d_geom, sizeof(BlockGeom) * c->n_local));
         CK(cudaMalloc(&c->d_sched, sizeof(unsigned int) * 2 * (c->n_local + 1)));
         CK(cudaMemset(c->d_sched, 0, sizeof(unsigned int) * 2 * (c->n_local + 1)));
-        if (const char* e = std::getenv("J3D_STORE_HINT")) c->store_hint = std::atoi(e) != 0;
         if (const char* e = std::getenv("J3D_XSECTOR")) c->xsector_ok = std::atoi(e) != 0;
         c->peer_base.assign(c->n_gpus, nullptr);
         build_static_tables(c);

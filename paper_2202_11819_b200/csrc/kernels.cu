@@ -769,7 +769,7 @@ static cudaError_t launch_t(const StencilLaunch& L, cudaStream_t st) {
     if (L.n_items <= 0) return cudaSuccess;
     stencil_tma_kernel<T><<<L.grid, T::THREADS, T::SMEM_BYTES, st>>>(
         L.descs, L.tmaps, L.tmaps_split, L.items, L.n_items, L.parity,
-        (L.faces ? 1 : 0) | (L.store_hint ? 2 : 0) | ((L.tma_mode & 3) << 2), L.sched);
+        (L.faces ? 1 : 0) | ((L.tma_mode & 3) << 2), L.sched);
     return cudaGetLastError();
 }
 

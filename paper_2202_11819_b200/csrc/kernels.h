@@ -24,7 +24,6 @@ struct StencilLaunch {
     int grid;    // persistent CTAs
     int kind;    // tile configuration (kernels.cu J3D_TILES)
     bool faces;  // any prologue/epilogue faces in this launch
-    bool store_hint;         // L2 evict_first policy on the output stores
     unsigned int* sched;     // device [2] scheduler counters (zero on entry; reset by the kernel)
 };
 
