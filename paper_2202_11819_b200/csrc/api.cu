@@ -1,0 +1,566 @@
+// api.cu -- the C ABI of include/jacobi3d.h.  Every entry point converts
+// exceptions into J3D_E* codes and a thread-local message; nothing throws
+// across the boundary.
+#include "context.h"
+
+using namespace j3d;
+
+namespace {
+
+static thread_local std::string g_err;
+
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        g_err.clear();
+        return f();
+    } catch (const Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return J3D_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return J3D_ECUDA;
+    }
+}
+
+int validate_cfg(const jacobi3d_config* c) {
+    if (!c) return fail(J3D_EINVAL, "config is NULL");
+    if (c->variant < J3D_UNFUSED || c->variant > J3D_FUSE_DIRECT) return fail(J3D_EINVAL, "unknown variant");
+    if (c->launch != J3D_PER_BLOCK && c->launch != J3D_BATCHED) return fail(J3D_EINVAL, "unknown launch mode");
+    if (c->exchange < J3D_XCHG_AUTO || c->exchange > J3D_XCHG_HOST) return fail(J3D_EINVAL, "unknown exchange backend");
+    if (c->n_gpus < 1 || c->rank < 0 || c->rank >= c->n_gpus) return fail(J3D_EINVAL, "rank / n_gpus out of range");
+    if (c->odf < 1) return fail(J3D_EINVAL, "odf must be >= 1");
+    if (c->reserved != 0 || (c->overlap != 0 && c->overlap != 1)) return fail(J3D_EINVAL, "bad overlap/reserved");
+    return J3D_OK;
+}
+
+
+}  // namespace
+
+// ======================================================================= C ABI
+extern "C" {
+
+const char* jacobi3d_last_error(void) { return g_err.c_str(); }
+
+int jacobi3d_plan(const jacobi3d_config* cfg, jacobi3d_plan_info* out) {
+    return guarded([&]() -> int {
+        if (!out) return fail(J3D_EINVAL, "out is NULL");
+        int rc = validate_cfg(cfg);
+        if (rc) return rc;
+        Plan P;
+        std::string msg;
+        rc = make_plan({cfg->gx, cfg->gy, cfg->gz}, {cfg->bx, cfg->by, cfg->bz}, cfg->odf, cfg->n_gpus, P, msg);
+        if (rc) return fail(rc, msg);
+        std::memset(out, 0, sizeof *out);
+        for (int a = 0; a < 3; ++a) {
+            out->gpu_grid[a] = P.gpu_grid[a];
+            out->blk_grid[a] = P.blk_grid[a];
+            out->blk_ext[a] = P.ext[a];
+        }
+        out->n_blocks = (int64_t)P.blocks.size();
+        // bytes: same layout as build_layout
+        const int64_t nx = P.ext[0], ny = P.ext[1], nz = P.ext[2];
+        const int64_t pitch = align_up(XOFF + nx + 1, PITCH_ALIGN);
+        const int64_t buf = align_up(pitch * (ny + 2) * (nz + 2) * 8, 256);
+        int64_t faces = 0;
+        for (int f = 0; f < 6; ++f) faces += 4 * align_up(face_cells(P.ext, f) * 8, 256);
+        out->bytes_per_gpu = 4096 + (int64_t)P.odf * (2 * buf + faces);
+        int32_t pmax = 0;
+        for (int r = 0; r < P.n_gpus; ++r) {
+            int32_t cnt = 0, loc = 0;
+            for (int64_t id : P.by_rank[r])
+                for (int f = 0; f < 6; ++f) {
+                    const int64_t nb = P.blocks[id].nbr[f];
+                    if (nb < 0) continue;
+                    if (P.blocks[nb].owner != r) cnt++;
+                    else loc++;
+                }
+            pmax = std::max(pmax, cnt);
+            if (r == cfg->rank) out->local_faces = loc;
+        }
+        out->peer_faces_max = pmax;
+        return J3D_OK;
+    });
+}
+
+int jacobi3d_nccl_unique_id(uint8_t out[128]) {
+    return guarded([&]() -> int {
+        if (!out) return fail(J3D_EINVAL, "out is NULL");
+        static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+        ncclUniqueId id;
+        NK(ncclGetUniqueId(&id));
+        std::memcpy(out, &id, 128);
+        return J3D_OK;
+    });
+}
+
+int jacobi3d_create(const jacobi3d_config* cfg, const uint8_t* nccl_uid, jacobi3d_t** out) {
+    if (out) *out = nullptr;
+    jacobi3d* c = nullptr;
+    int rc = guarded([&]() -> int {
+        if (!out) return fail(J3D_EINVAL, "out is NULL");
+        int rc2 = validate_cfg(cfg);
+        if (rc2) return rc2;
+        if (cfg->n_gpus > 1 && !nccl_uid) return fail(J3D_EINVAL, "nccl_uid required when n_gpus > 1");
+        c = new jacobi3d();
+        c->cfg = *cfg;
+        c->rank = cfg->rank;
+        c->n_gpus = cfg->n_gpus;
+        c->device = cfg->device;
+        std::string msg;
+        rc2 = make_plan({cfg->gx, cfg->gy, cfg->gz}, {cfg->bx, cfg->by, cfg->bz}, cfg->odf, cfg->n_gpus, c->plan, msg);
+        if (rc2) return fail(rc2, msg);
+        CK(cudaSetDevice(c->device));
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, c->device));
+        if (prop.major < 10) throw Error(J3D_EUNSUPPORTED, "this build targets sm_100a (B200)");
+        c->sms = prop.multiProcessorCount;
+        classify(c);
+        build_layout(c);
+        c->overlap = cfg->overlap && cfg->launch == J3D_BATCHED && c->n_gpus > 1 &&
+                     std::any_of(c->has_peer.begin(), c->has_peer.end(), [](uint8_t h) { return h != 0; });
+        CK(cudaMalloc(&c->arena, (size_t)c->arena_bytes));
+        CK(cudaMemset(c->arena, 0, 4096));
+        // face buffers start zeroed; done here, before any peer can map the
+        // arena, so it can never race with a peer's NVLink stores
+        CK(cudaMemset(c->arena + c->off_faces, 0, (size_t)(c->arena_bytes - c->off_faces)));
+        CK(cudaMalloc(&c->d_descs, sizeof(StencilDesc) * 2 * c->n_local));
+        CK(cudaMalloc(&c->d_tmaps, sizeof(CUtensorMap) * 2 * c->n_local));
+        CK(cudaMalloc(&c->d_tmaps_split, sizeof(CUtensorMap) * 4 * c->n_local));
+        CK(cudaMalloc(&c->d_pack, sizeof(CopyDesc) * 12 * c->n_local));
+        CK(cudaMalloc(&c->d_unpack, sizeof(CopyDesc) * 12 * c->n_local));
+        CK(cudaMalloc(&c->d_unpack_nccl, sizeof(CopyDesc) * 12 * c->n_local));
+        CK(cudaMalloc(&c->d_pack_peer, sizeof(CopyDesc) * 12 * c->n_local));
+        CK(cudaMalloc(&c->d_unpack_peer, sizeof(CopyDesc) * 12 * c->n_local));
+        CK(cudaMalloc(&c->d_pack_local, sizeof(CopyDesc) * 12 * c->n_local));
+        CK(cudaMalloc(&c->d_unpack_local, sizeof(CopyDesc) * 12 * c->n_local));
+        CK(cudaMalloc(&c->d_geom, sizeof(BlockGeom) * c->n_local));
+        CK(cudaMalloc(&c->d_sched, sizeof(unsigned int) * 2 * (c->n_local + 1)));
+        CK(cudaMemset(c->d_sched, 0, sizeof(unsigned int) * 2 * (c->n_local + 1)));
+        if (const char* e = std::getenv("J3D_XSECTOR")) c->xsector_ok = std::atoi(e) != 0;
+        c->peer_base.assign(c->n_gpus, nullptr);
+        build_static_tables(c);
+        build_tables(c);
+        CK(cudaStreamCreateWithFlags(&c->main, cudaStreamNonBlocking));
+        int lo_pr = 0, hi_pr = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo_pr, &hi_pr));
+        c->block_launches.assign(c->n_local, 0);
+        if (cfg->launch == J3D_PER_BLOCK) {
+            c->lo.assign(c->n_local, nullptr);
+            c->hi.assign(c->n_local, nullptr);
+            for (int l = 0; l < c->n_local; ++l) {
+                CK(cudaStreamCreateWithPriority(&c->lo[l], cudaStreamNonBlocking, lo_pr));
+                CK(cudaStreamCreateWithPriority(&c->hi[l], cudaStreamNonBlocking, hi_pr));
+            }
+        }
+        auto mk = [](cudaEvent_t* e) { CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming)); };
+        c->ev_st.assign(c->n_local, {nullptr, nullptr});
+        c->ev_pk.assign(c->n_local, {nullptr, nullptr});
+        c->ev_up.assign(c->n_local, {nullptr, nullptr});
+        for (int l = 0; l < c->n_local; ++l)
+            for (int p = 0; p < 2; ++p) {
+                mk(&c->ev_st[l][p]);
+                mk(&c->ev_pk[l][p]);
+                mk(&c->ev_up[l][p]);
+            }
+        mk(&c->ev_xw[0]);
+        mk(&c->ev_xw[1]);
+        for (int p = 0; p < 2; ++p) {
+            mk(&c->ev_ext[p]);
+            mk(&c->ev_comm[p]);
+        }
+        if (c->overlap) CK(cudaStreamCreateWithPriority(&c->xstream, cudaStreamNonBlocking, hi_pr));
+        mk(&c->ev_fork);
+        CK(cudaEventCreate(&c->ev_t0));
+        CK(cudaEventCreate(&c->ev_t1));
+        if (c->n_gpus > 1) {
+            ncclUniqueId id;
+            std::memcpy(&id, nccl_uid, 128);
+            NK(ncclCommInitRank(&c->comm, c->n_gpus, id, c->rank));
+            uint64_t h = 1469598103934665603ULL;  // FNV-1a of the unique id: a job-wide key
+            for (int i = 0; i < 128; ++i) h = (h ^ nccl_uid[i]) * 1099511628211ULL;
+            c->job_key = h;
+        }
+        if (c->host_needed) {
+            g_drv.load();
+            host_setup_own(c);
+        }
+        CK(cudaDeviceSynchronize());
+        *out = c;
+        return J3D_OK;
+    });
+    if (rc != J3D_OK && c) {
+        std::string keep = g_err;
+        destroy_ctx(c);
+        g_err = keep;
+    }
+    return rc;
+}
+
+int jacobi3d_ipc_export(jacobi3d_t* c, uint8_t* host_out, size_t cap, size_t* len) {
+    return guarded([&]() -> int {
+        if (!c || !len) return fail(J3D_EINVAL, "NULL argument");
+        *len = sizeof(IpcRecord);
+        if (!host_out || cap < sizeof(IpcRecord)) return fail(J3D_EINVAL, "buffer too small");
+        IpcRecord r;
+        std::memset(&r, 0, sizeof r);
+        r.magic = kIpcMagic;
+        r.rank = c->rank;
+        r.device = c->device;
+        r.arena_bytes = (uint64_t)c->arena_bytes;
+        CK(cudaSetDevice(c->device));
+        if (c->p2p_needed) CK(cudaIpcGetMemHandle(&r.handle, c->arena));
+        std::memcpy(host_out, &r, sizeof r);
+        return J3D_OK;
+    });
+}
+
+int jacobi3d_ipc_connect(jacobi3d_t* c, const uint8_t* all, size_t len_per_rank) {
+    return guarded([&]() -> int {
+        if (!c || !all) return fail(J3D_EINVAL, "NULL argument");
+        if (c->host_needed && !c->host_connected) {
+            CK(cudaSetDevice(c->device));
+            host_connect(c);
+        }
+        if (!c->p2p_needed) return J3D_OK;
+        if (len_per_rank != sizeof(IpcRecord)) return fail(J3D_EINVAL, "record size mismatch");
+        CK(cudaSetDevice(c->device));
+        for (int r : c->peer_ranks) {
+            IpcRecord rec;
+            std::memcpy(&rec, all + (size_t)r * len_per_rank, sizeof rec);
+            if (rec.magic != kIpcMagic || rec.rank != r || rec.arena_bytes != (uint64_t)c->arena_bytes)
+                return fail(J3D_EINVAL, "bad IPC record for rank " + std::to_string(r));
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, c->device, rec.device);
+            if (!can && rec.device != c->device)
+                return fail(J3D_EUNSUPPORTED, "device " + std::to_string(c->device) + " cannot access peer device " +
+                                                  std::to_string(rec.device));
+            void* p = nullptr;
+            CK(cudaIpcOpenMemHandle(&p, rec.handle, cudaIpcMemLazyEnablePeerAccess));
+            c->peer_base[r] = (char*)p;
+        }
+        c->p2p_connected = true;
+        drop_graphs(c);
+        build_tables(c);
+        CK(cudaDeviceSynchronize());
+        return J3D_OK;
+    });
+}
+
+int jacobi3d_init(jacobi3d_t* c, int kind, const double* p, uint64_t seed) {
+    return guarded([&]() -> int {
+        if (!c) return fail(J3D_EINVAL, "ctx is NULL");
+        if (kind < J3D_INIT_DEFAULT || kind > J3D_INIT_HASH) return fail(J3D_EINVAL, "unknown init kind");
+        if ((kind == J3D_INIT_CONST || kind == J3D_INIT_LINEAR) && !p) return fail(J3D_EINVAL, "params required");
+        if ((c->p2p_needed && !c->p2p_connected) || (c->host_needed && !c->host_connected))
+            return fail(J3D_ESTATE, "P2P / host exchange needs jacobi3d_ipc_export/jacobi3d_ipc_connect first");
+        CK(cudaSetDevice(c->device));
+        double pp[4] = {0, 0, 0, 0};
+        if (p) std::memcpy(pp, p, sizeof pp);
+        CK(launch_init(c->d_geom, c->n_local, (int)c->nx, (c->ny + 2) * (c->nz + 2), kind, pp, seed,
+                       c->cfg.boundary, c->cfg.gx, c->cfg.gy, c->cfg.gz, c->main));
+        count_launch(c, -1);
+        c->iter = 0;
+        c->iter_since_set = 0;
+        c->halos_stale = false;
+        // every collective state change ends with one exchange, which keeps the
+        // epoch-slot sequence alternating and fills the
+        // receive buffers the fused prologue reads
+        refresh(c, 0);
+        return J3D_OK;
+    });
+}
+
+int jacobi3d_refresh_halos(jacobi3d_t* c) {
+    return guarded([&]() -> int {
+        if (!c) return fail(J3D_EINVAL, "ctx is NULL");
+        CK(cudaSetDevice(c->device));
+        refresh(c, (int)(c->iter & 1));
+        c->halos_stale = false;
+        return J3D_OK;
+    });
+}
+
+static int block_local(jacobi3d* c, int64_t id, int* l) {
+    if (id < 0 || id >= (int64_t)c->plan.blocks.size()) return fail(J3D_EINVAL, "block id out of range");
+    const BlockPlan& b = c->plan.blocks[id];
+    if (b.owner != c->rank) return fail(J3D_ENOTLOCAL, "block " + std::to_string(id) + " is on rank " + std::to_string(b.owner));
+    *l = b.local;
+    return J3D_OK;
+}
+
+static cudaMemcpy3DParms owned_copy(jacobi3d* c, int l, int par, double* host, bool to_host) {
+    cudaMemcpy3DParms m;
+    std::memset(&m, 0, sizeof m);
+    double* dev = c->buf(l, par) + c->zs + c->pitch + XOFF;
+    cudaPitchedPtr d = make_cudaPitchedPtr(dev, (size_t)c->pitch * 8, (size_t)c->nx, (size_t)(c->ny + 2));
+    cudaPitchedPtr h = make_cudaPitchedPtr(host, (size_t)c->nx * 8, (size_t)c->nx, (size_t)c->ny);
+    if (to_host) {
+        m.srcPtr = d;
+        m.dstPtr = h;
+        m.kind = cudaMemcpyDeviceToHost;
+    } else {
+        m.srcPtr = h;
+        m.dstPtr = d;
+        m.kind = cudaMemcpyHostToDevice;
+    }
+    m.extent = make_cudaExtent((size_t)c->nx * 8, (size_t)c->ny, (size_t)c->nz);
+    return m;
+}
+
+int jacobi3d_set_block(jacobi3d_t* c, int64_t id, const double* host_in) {
+    return guarded([&]() -> int {
+        if (!c || !host_in) return fail(J3D_EINVAL, "NULL argument");
+        int l = 0;
+        int rc = block_local(c, id, &l);
+        if (rc) return rc;
+        CK(cudaSetDevice(c->device));
+        cudaMemcpy3DParms m = owned_copy(c, l, (int)(c->iter & 1), const_cast<double*>(host_in), false);
+        CK(cudaMemcpy3DAsync(&m, c->main));
+        wait_stream(c, c->main);
+        c->halos_stale = true;
+        c->iter_since_set = 0;
+        return J3D_OK;
+    });
+}
+
+int jacobi3d_get_block(jacobi3d_t* c, int64_t id, double* host_out) {
+    return guarded([&]() -> int {
+        if (!c || !host_out) return fail(J3D_EINVAL, "NULL argument");
+        int l = 0;
+        int rc = block_local(c, id, &l);
+        if (rc) return rc;
+        CK(cudaSetDevice(c->device));
+        cudaMemcpy3DParms m = owned_copy(c, l, (int)(c->iter & 1), host_out, true);
+        CK(cudaMemcpy3DAsync(&m, c->main));
+        wait_stream(c, c->main);
+        return J3D_OK;
+    });
+}
+
+int jacobi3d_get_region(jacobi3d_t* c, int64_t id, const int64_t lo[3], const int64_t ext[3], double* host_out) {
+    return guarded([&]() -> int {
+        if (!c || !lo || !ext || !host_out) return fail(J3D_EINVAL, "NULL argument");
+        int l = 0;
+        int rc = block_local(c, id, &l);
+        if (rc) return rc;
+        const int64_t n[3] = {c->nx, c->ny, c->nz};
+        for (int a = 0; a < 3; ++a)
+            if (lo[a] < 0 || ext[a] < 1 || lo[a] + ext[a] > n[a]) return fail(J3D_EINVAL, "region outside the block");
+        CK(cudaSetDevice(c->device));
+        cudaMemcpy3DParms m;
+        std::memset(&m, 0, sizeof m);
+        double* dev = c->buf(l, (int)(c->iter & 1)) + (lo[2] + 1) * c->zs + (lo[1] + 1) * c->pitch + XOFF + lo[0];
+        m.srcPtr = make_cudaPitchedPtr(dev, (size_t)c->pitch * 8, (size_t)ext[0], (size_t)(c->ny + 2));
+        m.dstPtr = make_cudaPitchedPtr(host_out, (size_t)ext[0] * 8, (size_t)ext[0], (size_t)ext[1]);
+        m.kind = cudaMemcpyDeviceToHost;
+        m.extent = make_cudaExtent((size_t)ext[0] * 8, (size_t)ext[1], (size_t)ext[2]);
+        CK(cudaMemcpy3DAsync(&m, c->main));
+        wait_stream(c, c->main);
+        return J3D_OK;
+    });
+}
+
+int jacobi3d_block_info(jacobi3d_t* c, int64_t id, int64_t origin[3], int64_t extent[3], int32_t* owner) {
+    return guarded([&]() -> int {
+        if (!c) return fail(J3D_EINVAL, "ctx is NULL");
+        if (id < 0 || id >= (int64_t)c->plan.blocks.size()) return fail(J3D_EINVAL, "block id out of range");
+        const BlockPlan& b = c->plan.blocks[id];
+        for (int a = 0; a < 3; ++a) {
+            if (origin) origin[a] = b.origin[a];
+            if (extent) extent[a] = c->plan.ext[a];
+        }
+        if (owner) *owner = b.owner;
+        return J3D_OK;
+    });
+}
+
+int jacobi3d_iterate(jacobi3d_t* c, int64_t n) {
+    return guarded([&]() -> int {
+        if (!c) return fail(J3D_EINVAL, "ctx is NULL");
+        if (n < 0) return fail(J3D_EINVAL, "n must be >= 0");
+        CK(cudaSetDevice(c->device));
+        do_iterate(c, n);
+        return J3D_OK;
+    });
+}
+
+int jacobi3d_synchronize(jacobi3d_t* c) {
+    return guarded([&]() -> int {
+        if (!c) return fail(J3D_EINVAL, "ctx is NULL");
+        CK(cudaSetDevice(c->device));
+        wait_stream(c, c->main);
+        CK(cudaDeviceSynchronize());
+        if (c->comm) {
+            ncclResult_t ar = ncclSuccess;
+            NK(ncclCommGetAsyncError(c->comm, &ar));
+            NK(ar);
+        }
+        return J3D_OK;
+    });
+}
+
+int jacobi3d_residual(jacobi3d_t* c, double* out) {
+    return guarded([&]() -> int {
+        if (!c || !out) return fail(J3D_EINVAL, "NULL argument");
+        if (c->iter_since_set < 1) return fail(J3D_ESTATE, "residual needs >= 1 iteration since init/set_block");
+        CK(cudaSetDevice(c->device));
+        unsigned long long* acc = (unsigned long long*)(c->arena + c->off_scratch);
+        CK(cudaMemsetAsync(acc, 0, 8, c->main));
+        CK(launch_residual(c->d_geom, c->n_local, (int)(c->iter & 1), acc, c->sms, c->main));
+        count_launch(c, -1);
+        if (c->n_gpus > 1) NK(ncclAllReduce(acc, acc, 1, ncclUint64, ncclMax, c->comm, c->main));
+        unsigned long long h = 0;
+        CK(cudaMemcpyAsync(&h, acc, 8, cudaMemcpyDeviceToHost, c->main));
+        wait_stream(c, c->main);
+        double d;
+        std::memcpy(&d, &h, 8);
+        *out = d;
+        return J3D_OK;
+    });
+}
+
+int jacobi3d_checksum(jacobi3d_t* c, uint64_t* out) {
+    return guarded([&]() -> int {
+        if (!c || !out) return fail(J3D_EINVAL, "NULL argument");
+        CK(cudaSetDevice(c->device));
+        unsigned long long* acc = (unsigned long long*)(c->arena + c->off_scratch + 8);
+        CK(cudaMemsetAsync(acc, 0, 8, c->main));
+        CK(launch_checksum(c->d_geom, c->n_local, (int)(c->iter & 1), c->cfg.gx, c->cfg.gy, acc, c->sms, c->main));
+        count_launch(c, -1);
+        if (c->n_gpus > 1) NK(ncclAllReduce(acc, acc, 1, ncclUint64, ncclSum, c->comm, c->main));
+        unsigned long long h = 0;
+        CK(cudaMemcpyAsync(&h, acc, 8, cudaMemcpyDeviceToHost, c->main));
+        wait_stream(c, c->main);
+        *out = (uint64_t)h;
+        return J3D_OK;
+    });
+}
+
+int jacobi3d_time(jacobi3d_t* c, int64_t warmup, int64_t iters, double* ms) {
+    return guarded([&]() -> int {
+        if (!c || !ms || iters < 1 || warmup < 0) return fail(J3D_EINVAL, "bad argument");
+        CK(cudaSetDevice(c->device));
+        do_iterate(c, warmup);
+        wait_stream(c, c->main);
+        CK(cudaDeviceSynchronize());
+        nccl_barrier(c);
+        CK(cudaEventRecord(c->ev_t0, c->main));
+        do_iterate(c, iters);
+        CK(cudaEventRecord(c->ev_t1, c->main));
+        wait_stream(c, c->main);
+        CK(cudaEventSynchronize(c->ev_t1));
+        float f = 0;
+        CK(cudaEventElapsedTime(&f, c->ev_t0, c->ev_t1));
+        *ms = (double)f / (double)iters;
+        return J3D_OK;
+    });
+}
+
+int jacobi3d_get_stats(jacobi3d_t* c, jacobi3d_stats* out) {
+    return guarded([&]() -> int {
+        if (!c || !out) return fail(J3D_EINVAL, "NULL argument");
+        std::memset(out, 0, sizeof *out);
+        out->iterations = c->iter;
+        out->kernel_launches = c->stat_launches;
+        out->graph_launches = c->stat_graph_launches;
+        out->last_graph_parity = c->stat_last_parity;
+        int64_t mx = 0;
+        for (int64_t v : c->block_launches) mx = std::max(mx, v);
+        out->launches_per_iter_block = c->stat_iters > 0 ? mx / c->stat_iters : 0;
+        return J3D_OK;
+    });
+}
+
+int jacobi3d_reset_stats(jacobi3d_t* c) {
+    if (!c) return fail(J3D_EINVAL, "ctx is NULL");
+    c->stat_launches = c->stat_graph_launches = c->stat_iters = 0;
+    c->stat_last_parity = -1;
+    std::fill(c->block_launches.begin(), c->block_launches.end(), 0);
+    return J3D_OK;
+}
+
+int jacobi3d_profile_enable(jacobi3d_t* c, int enable) {
+    return guarded([&]() -> int {
+        if (!c) return fail(J3D_EINVAL, "ctx is NULL");
+        CK(cudaSetDevice(c->device));
+        CK(cudaDeviceSynchronize());
+        for (auto& pr : c->prof_events) {
+            c->ev_pool.push_back(pr.first);
+            c->ev_pool.push_back(pr.second);
+        }
+        c->prof_events.clear();
+        c->prof = enable != 0;
+        c->prof_ms = c->prof_bytes = c->prof_pending_bytes = 0;
+        c->prof_launches = 0;
+        return J3D_OK;
+    });
+}
+
+int jacobi3d_profile_read(jacobi3d_t* c, double* total_ms, int64_t* launches, double* bytes) {
+    return guarded([&]() -> int {
+        if (!c) return fail(J3D_EINVAL, "ctx is NULL");
+        CK(cudaSetDevice(c->device));
+        CK(cudaDeviceSynchronize());
+        for (auto& pr : c->prof_events) {
+            float f = 0;
+            CK(cudaEventElapsedTime(&f, pr.first, pr.second));
+            c->prof_ms += f;
+            c->prof_launches += 1;
+            c->ev_pool.push_back(pr.first);
+            c->ev_pool.push_back(pr.second);
+        }
+        c->prof_events.clear();
+        c->prof_bytes += c->prof_pending_bytes;
+        c->prof_pending_bytes = 0;
+        if (total_ms) *total_ms = c->prof_ms;
+        if (launches) *launches = c->prof_launches;
+        if (bytes) *bytes = c->prof_bytes;
+        return J3D_OK;
+    });
+}
+
+int jacobi3d_set_skip_exchange(jacobi3d_t* c, int skip) {
+    if (!c) return fail(J3D_EINVAL, "ctx is NULL");
+    if ((skip != 0) != c->skip_exchange) drop_graphs(c);
+    c->skip_exchange = skip != 0;
+    return J3D_OK;
+}
+
+int jacobi3d_div7_selftest(uint64_t n, uint64_t seed, uint64_t* mismatches, double* example) {
+    return guarded([&]() -> int {
+        if (!mismatches) return fail(J3D_EINVAL, "NULL argument");
+        int dev = 0, sms = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        unsigned long long* d = nullptr;
+        CK(cudaMalloc(&d, 64));
+        CK(cudaMemset(d, 0, 64));
+        cudaError_t e = launch_div7_selftest(n, seed, d, (double*)(d + 1), sms, 0);
+        unsigned long long h[4] = {0, 0, 0, 0};
+        if (e == cudaSuccess) e = cudaMemcpy(h, d, 32, cudaMemcpyDeviceToHost);
+        cudaFree(d);
+        CK(e);
+        *mismatches = h[0];
+        if (example) std::memcpy(example, h + 1, 24);
+        return J3D_OK;
+    });
+}
+
+int jacobi3d_destroy(jacobi3d_t* c) {
+    return guarded([&]() -> int {
+        destroy_ctx(c);
+        return J3D_OK;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,351 @@
+// setup.cu -- arena layout, face classification, device descriptor tables, TMA tensor maps and the work-item list of a context.
+#include "context.h"
+
+using namespace j3d;
+
+namespace j3d {
+
+Driver g_drv;
+
+void build_layout(jacobi3d* c) {
+    const Plan& P = c->plan;
+    c->nx = P.ext[0];
+    c->ny = P.ext[1];
+    c->nz = P.ext[2];
+    c->pitch = align_up(XOFF + c->nx + 1, PITCH_ALIGN);
+    c->zs = c->pitch * (c->ny + 2);
+    c->buf_elems = c->zs * (c->nz + 2);
+    c->buf_bytes = align_up(c->buf_elems * 8, 256);
+    for (int f = 0; f < 6; ++f) c->face_bytes[f] = align_up(face_cells(P.ext, f) * 8, 256);
+    c->faces_per_block_bytes = 0;
+    for (int f = 0; f < 6; ++f) c->faces_per_block_bytes += 4 * c->face_bytes[f];  // send/recv x 2 parities
+    c->off_flags = 0;
+    c->off_scratch = 2048;
+    c->off_bufs = 4096;
+    c->off_faces = c->off_bufs + (int64_t)c->n_local * 2 * c->buf_bytes;
+    c->arena_bytes = c->off_faces + (int64_t)c->n_local * c->faces_per_block_bytes;
+}
+
+void classify(jacobi3d* c) {
+    const Plan& P = c->plan;
+    c->gid = P.by_rank[c->rank];
+    c->n_local = (int)c->gid.size();
+    c->kind.assign(c->n_local, {});
+    c->nbr_local.assign(c->n_local, {});
+    c->has_peer.assign(c->n_local, 0);
+    int xchg = c->cfg.exchange == J3D_XCHG_AUTO ? J3D_XCHG_P2P : c->cfg.exchange;
+    std::vector<int> peers;
+    for (int l = 0; l < c->n_local; ++l) {
+        const BlockPlan& b = P.blocks[c->gid[l]];
+        for (int f = 0; f < 6; ++f) {
+            if (b.nbr[f] < 0) {
+                c->kind[l][f] = DIRICHLET;
+                c->nbr_local[l][f] = -1;
+            } else {
+                const BlockPlan& n = P.blocks[b.nbr[f]];
+                c->nbr_local[l][f] = n.local;
+                if (n.owner == c->rank) {
+                    c->kind[l][f] = LOCAL;
+                } else {
+                    c->kind[l][f] = xchg == J3D_XCHG_NCCL ? PEER_NCCL : xchg == J3D_XCHG_HOST ? PEER_HOST : PEER_P2P;
+                    if (xchg == J3D_XCHG_HOST) c->host_needed = true;
+                    c->has_peer[l] = 1;
+                    if (std::find(peers.begin(), peers.end(), n.owner) == peers.end()) peers.push_back(n.owner);
+                    if (xchg == J3D_XCHG_P2P) c->p2p_needed = true;
+                }
+            }
+        }
+    }
+    std::sort(peers.begin(), peers.end());
+    c->peer_ranks = peers;
+    c->order.clear();
+    for (int l = 0; l < c->n_local; ++l)
+        if (c->has_peer[l]) c->order.push_back(l);
+    for (int l = 0; l < c->n_local; ++l)
+        if (!c->has_peer[l]) c->order.push_back(l);
+    if (const char* e = std::getenv("J3D_ORDER_SEED")) {  // test hook: perturbed launch order
+        uint64_t st = std::strtoull(e, nullptr, 10) * 0x9E3779B97F4A7C15ULL + 1;
+        for (int i = (int)c->order.size() - 1; i > 0; --i) {
+            st ^= st << 13; st ^= st >> 7; st ^= st << 17;
+            std::swap(c->order[i], c->order[(int)(st % (uint64_t)(i + 1))]);
+        }
+    }
+}
+
+// Source of the ghost values of face f of local block l for buffer parity par
+// (what an unpack or a fused prologue reads).
+FaceRef recv_src(const jacobi3d* c, int l, int f, int par) {
+    if (c->kind[l][f] == LOCAL)  // same GPU: read the neighbour's send buffer in place
+        return c->contiguous(c->face_buf(c->nbr_local[l][f], f ^ 1, par, false), f);
+    return c->contiguous(c->face_buf(l, f, par, true), f);
+}
+
+// Destination of the pack of face f of local block l for parity par.
+FaceRef pack_dst(const jacobi3d* c, int l, int f, int par) {
+    if (c->kind[l][f] == PEER_P2P) {  // GPU-aware: straight into the peer's receive buffer (NVLink)
+        const int r = c->plan.blocks[c->plan.blocks[c->gid[l]].nbr[f]].owner;
+        return c->contiguous(c->face_buf(c->nbr_local[l][f], f ^ 1, par, true, r), f);
+    }
+    return c->contiguous(c->face_buf(l, f, par, false), f);
+}
+
+void build_tables(jacobi3d* c) {
+    const int nl = c->n_local;
+    const int v = c->cfg.variant;
+    // ---- stencil descriptors [2*l + p]
+    std::vector<StencilDesc> descs(2 * nl);
+    c->faces_fused = false;
+    for (int l = 0; l < nl; ++l)
+        for (int p = 0; p < 2; ++p) {
+            const int q = p ^ 1;
+            StencilDesc& d = descs[2 * l + p];
+            std::memset(&d, 0, sizeof d);
+            d.in = c->buf(l, p);
+            d.out = c->buf(l, q);
+            d.nx = (int32_t)c->nx;
+            d.ny = (int32_t)c->ny;
+            d.nz = (int32_t)c->nz;
+            d.pitch = c->pitch;
+            d.zs = c->zs;
+            if (v == J3D_FUSE_C || v == J3D_FUSE_DIRECT) {
+                for (int f = 0; f < 6; ++f) {
+                    const int k = c->kind[l][f];
+                    if (k == DIRICHLET) continue;
+                    bool direct = v == J3D_FUSE_DIRECT && (k == LOCAL || k == PEER_P2P);
+                    if (direct) {
+                        const int r = k == LOCAL ? -1 : c->plan.blocks[c->plan.blocks[c->gid[l]].nbr[f]].owner;
+                        if (k == PEER_P2P && !c->p2p_connected) continue;  // filled after ipc_connect
+                        d.epi[f] = c->layer(c->buf(c->nbr_local[l][f], q, r), f ^ 1, true);
+                        d.epi_mask |= 1u << f;
+                        if (f < 2 && (c->nx % 4) == 0 && c->xsector_ok) d.xsector |= 1u << f;  // whole-sector x-ghost stores
+                    } else if (v == J3D_FUSE_DIRECT) {
+                        // NCCL face of the direct variant: epilogue packs into the
+                        // send buffer; after the exchange a batched unpack kernel
+                        // writes the received face into the ghost layer (keeps the
+                        // stencil's prologue empty)
+                        d.epi[f] = pack_dst(c, l, f, q);
+                        d.epi_mask |= 1u << f;
+                    } else {
+                        if (k == PEER_P2P && !c->p2p_connected) continue;
+                        d.epi[f] = pack_dst(c, l, f, q);
+                        d.epi_mask |= 1u << f;
+                        d.pro[f] = recv_src(c, l, f, p);
+                        d.pro_mask |= 1u << f;
+                    }
+                }
+                if (d.epi_mask | d.pro_mask) c->faces_fused = true;
+            }
+        }
+    CK(cudaMemcpy(c->d_descs, descs.data(), descs.size() * sizeof(StencilDesc), cudaMemcpyHostToDevice));
+
+    // ---- pack / unpack copy descriptors [(q*nl + l)*6 + f]
+    std::vector<CopyDesc> pack(2 * nl * 6), unpack(2 * nl * 6);
+    for (int q = 0; q < 2; ++q)
+        for (int l = 0; l < nl; ++l)
+            for (int f = 0; f < 6; ++f) {
+                CopyDesc& pk = pack[(q * nl + l) * 6 + f];
+                CopyDesc& up = unpack[(q * nl + l) * 6 + f];
+                std::memset(&pk, 0, sizeof pk);
+                std::memset(&up, 0, sizeof up);
+                const int k = c->kind[l][f];
+                if (k == DIRICHLET) continue;
+                if (k == PEER_P2P && !c->p2p_connected) continue;
+                pk.src = c->layer(c->buf(l, q), f, false);
+                pk.dst = pack_dst(c, l, f, q);
+                pk.na = (int32_t)c->face_na(f);
+                pk.nb = (int32_t)c->face_nb(f);
+                up.src = recv_src(c, l, f, q);
+                up.dst = c->layer(c->buf(l, q), f, true);
+                up.na = pk.na;
+                up.nb = pk.nb;
+            }
+    CK(cudaMemcpy(c->d_pack, pack.data(), pack.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_unpack, unpack.data(), unpack.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
+    // NCCL faces only (direct variant's post-exchange unpack)
+    c->direct_nccl_unpack = false;
+    for (int q = 0; q < 2; ++q)
+        for (int l = 0; l < nl; ++l)
+            for (int f = 0; f < 6; ++f) {
+                CopyDesc& up = unpack[(q * nl + l) * 6 + f];
+                if (!via_buffers(c->kind[l][f])) std::memset(&up, 0, sizeof up);
+                else if (v == J3D_FUSE_DIRECT) c->direct_nccl_unpack = true;
+            }
+    CK(cudaMemcpy(c->d_unpack_nccl, unpack.data(), unpack.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
+    // peer-only / local-only tables for the overlap mode
+    {
+        std::vector<CopyDesc> pk_peer(pack), up_peer(2 * nl * 6), pk_loc(pack), up_loc(2 * nl * 6);
+        std::vector<CopyDesc> up_all(2 * nl * 6);
+        for (int q = 0; q < 2; ++q)
+            for (int l = 0; l < nl; ++l)
+                for (int f = 0; f < 6; ++f) {
+                    const int i = (q * nl + l) * 6 + f;
+                    const int k = c->kind[l][f];
+                    CopyDesc up;
+                    std::memset(&up, 0, sizeof up);
+                    if (k != DIRICHLET && !(k == PEER_P2P && !c->p2p_connected)) {
+                        up.src = recv_src(c, l, f, q);
+                        up.dst = c->layer(c->buf(l, q), f, true);
+                        up.na = (int32_t)c->face_na(f);
+                        up.nb = (int32_t)c->face_nb(f);
+                    }
+                    const bool peer = is_peer_kind(k);
+                    if (!peer) std::memset(&pk_peer[i], 0, sizeof(CopyDesc));
+                    if (peer || k == DIRICHLET) std::memset(&pk_loc[i], 0, sizeof(CopyDesc));
+                    if (peer) up_peer[i] = up;
+                    else if (k == LOCAL) up_loc[i] = up;
+                    if (!peer && k != LOCAL) std::memset(&up_peer[i], 0, sizeof(CopyDesc));
+                }
+        for (auto& d : up_peer) if (d.na == 0) std::memset(&d, 0, sizeof d);
+        CK(cudaMemcpy(c->d_pack_peer, pk_peer.data(), pk_peer.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->d_unpack_peer, up_peer.data(), up_peer.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->d_pack_local, pk_loc.data(), pk_loc.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->d_unpack_local, up_loc.data(), up_loc.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
+    }
+}
+
+void build_static_tables(jacobi3d* c) {
+    const int nl = c->n_local;
+    // ---- tensor maps [2*l + p] over each input buffer
+    g_drv.load();
+    // 192x22 tiles (11 consumer warps, 5-stage ring, 1 CTA/SM) when they divide
+    // the block width, else 128x30 (15 consumer warps) for wide blocks and
+    // 64x16 (2 CTAs/SM, 6 stages) for narrow ones.  Bench sweeps: profiles/.
+    c->tile_kind = (c->nx % 192 == 0) ? 0 : c->nx >= 128 ? 1 : 4;
+    {  // small grids: the wide tiles cannot keep every SM busy -> 64x16, 2 CTAs/SM
+        const TileShape t = tile_shape(c->tile_kind);
+        const int64_t tiles = ((c->nx + t.tx - 1) / t.tx) * ((c->ny + t.ty - 1) / t.ty) * nl;
+        const int64_t max_items = tiles * std::max<int64_t>(1, c->nz / 24);
+        if (c->tile_kind != 4 && max_items < 4LL * c->sms) c->tile_kind = 4;
+    }
+    if (const char* e = std::getenv("J3D_TILE")) {  // tuning override (bench sweeps)
+        const int k = std::atoi(e);
+        if (k >= 0 && k < num_tile_kinds()) c->tile_kind = k;
+    }
+    const TileShape ts = tile_shape(c->tile_kind);
+    std::vector<CUtensorMap> maps(2 * nl);
+    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    if (const char* e = std::getenv("J3D_L2PROMO")) {  // tuning override
+        const int v = std::atoi(e);
+        promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+              : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    }
+    for (int l = 0; l < nl; ++l)
+        for (int p = 0; p < 2; ++p) {
+            cuuint64_t dims[3] = {(cuuint64_t)(XOFF + c->nx + 1), (cuuint64_t)(c->ny + 2), (cuuint64_t)(c->nz + 2)};  // up to the +x ghost: the row padding is never fetched (TMA zero-fills beyond)
+            cuuint64_t strides[2] = {(cuuint64_t)(c->pitch * 8), (cuuint64_t)(c->zs * 8)};
+            cuuint32_t box[3] = {(cuuint32_t)stencil_box_w(c->tile_kind), (cuuint32_t)stencil_box_h(c->tile_kind), 1};
+            cuuint32_t es[3] = {1, 1, 1};
+            DK(g_drv.encode(&maps[2 * l + p], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->buf(l, p), dims, strides, box, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+        }
+    CK(cudaMemcpy(c->d_tmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+    // split maps: box heights 2 and H-4 (for the L2-policy split loads)
+    std::vector<CUtensorMap> maps2(4 * nl);
+    for (int l = 0; l < nl; ++l)
+        for (int p = 0; p < 2; ++p)
+            for (int h = 0; h < 2; ++h) {
+                cuuint64_t dims[3] = {(cuuint64_t)(XOFF + c->nx + 1), (cuuint64_t)(c->ny + 2), (cuuint64_t)(c->nz + 2)};  // up to the +x ghost: the row padding is never fetched (TMA zero-fills beyond)
+                cuuint64_t strides[2] = {(cuuint64_t)(c->pitch * 8), (cuuint64_t)(c->zs * 8)};
+                const int H = stencil_box_h(c->tile_kind);
+                cuuint32_t box[3] = {(cuuint32_t)stencil_box_w(c->tile_kind), (cuuint32_t)(h == 0 ? 2 : std::max(1, H - 4)), 1};
+                cuuint32_t es[3] = {1, 1, 1};
+                DK(g_drv.encode(&maps2[(2 * l + p) * 2 + h], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->buf(l, p), dims,
+                                strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+            }
+    CK(cudaMemcpy(c->d_tmaps_split, maps2.data(), maps2.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+    if (const char* e = std::getenv("J3D_TMA_HINT")) c->tma_mode = std::atoi(e) & 3;
+    if (c->tma_mode == 3 && stencil_box_h(c->tile_kind) < 6) c->tma_mode = 0;
+
+    // ---- work items: per block, z-chunk outer, then ty, tx (x fastest), peer-face blocks first
+    int occ = 1;
+    CK(stencil_occupancy(c->tile_kind, false, &occ));
+    occ = std::max(1, occ);
+    c->grid_cap = c->sms * occ;
+    const int64_t ntx = (c->nx + ts.tx - 1) / ts.tx, nty = (c->ny + ts.ty - 1) / ts.ty;
+    const int64_t tiles = ntx * nty * nl;
+    // z chunks of ~96 planes: items are handed out dynamically in list order
+    // (z chunk outer, then tiles), so x/y-neighbouring tiles -- whose halos
+    // overlap -- run concurrently and share halo rows through L2, while each
+    // chunk re-reads only 2 extra planes (2% at 96).  Measured sweep: 96
+    // beats 32/64/128/full depth (profiles/).
+    int64_t best_zc = std::max<int64_t>(1, (c->nz + 95) / 96);
+    // small problems: shorter chunks until there are >= 6 items per CTA slot
+    // (at least 24 planes per chunk): the last round of items is then short
+    // (measured: 96^3 blocks, ODF 64: 198 -> 225 GLUPS)
+    while (tiles * best_zc < 6 * (int64_t)c->grid_cap && c->nz / (best_zc + 1) >= 24) ++best_zc;
+    if (const char* e = std::getenv("J3D_ZCHUNK")) {  // tuning override: planes per z chunk
+        const int64_t L = std::atoll(e);
+        if (L > 0) best_zc = std::max<int64_t>(1, (c->nz + L - 1) / L);
+    }
+    int tile_order = 0;  // tuning override: tile order inside a z chunk
+    if (const char* e = std::getenv("J3D_TILE_ORDER")) tile_order = std::atoi(e);
+    std::vector<WorkItem> items;
+    c->item_begin.assign(nl, 0);
+    c->item_count.assign(nl, 0);
+    auto is_peer = [&](int l, int f) { return is_peer_kind(c->kind[l][f]); };
+    auto exterior = [&](const WorkItem& w) {  // does the item compute a cell adjacent to a peer face?
+        const int l = w.blk;
+        return (is_peer(l, 0) && w.tx == 0) || (is_peer(l, 1) && w.tx == ntx - 1) ||
+               (is_peer(l, 2) && w.ty == 0) || (is_peer(l, 3) && w.ty == nty - 1) ||
+               (is_peer(l, 4) && w.z0 == 0) || (is_peer(l, 5) && w.z1 == c->nz);
+    };
+    for (int l : c->order) {
+        c->item_begin[l] = (int)items.size();
+        for (int64_t zc = 0; zc < best_zc; ++zc) {
+            const int z0 = (int)(c->nz * zc / best_zc), z1 = (int)(c->nz * (zc + 1) / best_zc);
+            if (z1 <= z0) continue;
+            if (tile_order == 1) {  // y fastest
+                for (int64_t tx = 0; tx < ntx; ++tx)
+                    for (int64_t ty = 0; ty < nty; ++ty)
+                        items.push_back(WorkItem{l, (int16_t)tx, (int16_t)ty, z0, z1});
+            } else if (tile_order >= 2) {  // bands of `tile_order` tile rows, column-major inside a band
+                for (int64_t b0 = 0; b0 < nty; b0 += tile_order)
+                    for (int64_t tx = 0; tx < ntx; ++tx)
+                        for (int64_t ty = b0; ty < std::min<int64_t>(nty, b0 + tile_order); ++ty)
+                            items.push_back(WorkItem{l, (int16_t)tx, (int16_t)ty, z0, z1});
+            } else {  // x fastest
+                for (int64_t ty = 0; ty < nty; ++ty)
+                    for (int64_t tx = 0; tx < ntx; ++tx)
+                        items.push_back(WorkItem{l, (int16_t)tx, (int16_t)ty, z0, z1});
+            }
+        }
+        c->item_count[l] = (int)items.size() - c->item_begin[l];
+    }
+    c->n_ext = 0;
+    if (c->overlap) {  // BATCHED only: exterior items of every block first (stable order otherwise)
+        std::stable_partition(items.begin(), items.end(), exterior);
+        c->n_ext = (int)std::count_if(items.begin(), items.end(), exterior);
+    }
+    c->n_items = (int)items.size();
+    c->item_cells.assign(items.size() + 1, 0);
+    for (size_t i = 0; i < items.size(); ++i) {
+        const WorkItem& w = items[i];
+        const int64_t ex = std::min<int64_t>(ts.tx, c->nx - (int64_t)w.tx * ts.tx);
+        const int64_t ey = std::min<int64_t>(ts.ty, c->ny - (int64_t)w.ty * ts.ty);
+        c->item_cells[i + 1] = c->item_cells[i] + ex * ey * (w.z1 - w.z0);
+    }
+    CK(cudaMalloc(&c->d_items, std::max<size_t>(1, items.size()) * sizeof(WorkItem)));
+    CK(cudaMemcpy(c->d_items, items.data(), items.size() * sizeof(WorkItem), cudaMemcpyHostToDevice));
+
+    // ---- block geometry
+    std::vector<BlockGeom> geo(nl);
+    for (int l = 0; l < nl; ++l) {
+        const BlockPlan& b = c->plan.blocks[c->gid[l]];
+        geo[l].buf[0] = c->buf(l, 0);
+        geo[l].buf[1] = c->buf(l, 1);
+        geo[l].ox = b.origin[0];
+        geo[l].oy = b.origin[1];
+        geo[l].oz = b.origin[2];
+        geo[l].nx = (int32_t)c->nx;
+        geo[l].ny = (int32_t)c->ny;
+        geo[l].nz = (int32_t)c->nz;
+        geo[l].pitch = c->pitch;
+        geo[l].zs = c->zs;
+    }
+    CK(cudaMemcpy(c->d_geom, geo.data(), geo.size() * sizeof(BlockGeom), cudaMemcpyHostToDevice));
+}
+
+
+}  // namespace j3d
