@@ -139,6 +139,7 @@ int jacobi3d_create(const jacobi3d_config* cfg, const uint8_t* nccl_uid, jacobi3
         CK(cudaMalloc(&c->d_pack, sizeof(CopyDesc) * 12 * c->n_local));
         CK(cudaMalloc(&c->d_unpack, sizeof(CopyDesc) * 12 * c->n_local));
         CK(cudaMalloc(&c->d_unpack_nccl, sizeof(CopyDesc) * 12 * c->n_local));
+        CK(cudaMalloc(&c->d_push, sizeof(CopyDesc) * 12 * c->n_local));
         CK(cudaMalloc(&c->d_pack_peer, sizeof(CopyDesc) * 12 * c->n_local));
         CK(cudaMalloc(&c->d_unpack_peer, sizeof(CopyDesc) * 12 * c->n_local));
         CK(cudaMalloc(&c->d_pack_local, sizeof(CopyDesc) * 12 * c->n_local));

@@ -164,7 +164,9 @@ struct jacobi3d {
     int n_ext = 0;                             // items [0, n_ext) touch a peer face
     cudaStream_t xstream = nullptr;            // exchange stream (overlap mode)
     std::array<cudaEvent_t, 2> ev_ext{}, ev_comm{};
-    bool direct_nccl_unpack = false;
+    bool direct_nccl_unpack = false;             // direct variant: post-exchange unpack of buffered faces
+    bool direct_push = false;                    // direct variant: peer x faces pushed send -> peer recv
+    CopyDesc* d_push = nullptr;
     BlockGeom* d_geom = nullptr;
     unsigned int* d_sched = nullptr;            // [2*(n_local+1)] stencil work counters
     bool xsector_ok = true;  // J3D_XSECTOR=0 disables whole-sector x-ghost stores (tuning)

@@ -133,6 +133,7 @@ void enqueue_iteration(jacobi3d* c, int p, bool first, bool last) {
             CK(cudaEventRecord(c->ev_ext[q], c->main));
             CK(cudaStreamWaitEvent(c->xstream, c->ev_ext[q], 0));
             if (unf) copies(c, c->d_pack_peer, q, -1, 0, true, c->xstream);
+            else if (c->direct_push) copies(c, c->d_push, q, -1, 0, true, c->xstream);
             cross_gpu_exchange(c, q, q, c->xstream);
             if (unf) copies(c, c->d_unpack_peer, q, -1, 0, true, c->xstream);
             else if (c->direct_nccl_unpack) copies(c, c->d_unpack_nccl, q, -1, 0, true, c->xstream);
@@ -147,6 +148,7 @@ void enqueue_iteration(jacobi3d* c, int p, bool first, bool last) {
         }
         stencil(c, 0, c->n_items, p, c->main, -1);
         if (unf) copies(c, c->d_pack, q, -1, 0, true, c->main);
+        else if (c->direct_push && !c->skip_exchange) copies(c, c->d_push, q, -1, 0, true, c->main);
         cross_gpu_exchange(c, q, q, c->main);
         if (unf) copies(c, c->d_unpack, q, -1, 0, true, c->main);
         else if (c->direct_nccl_unpack && !c->skip_exchange) copies(c, c->d_unpack_nccl, q, -1, 0, true, c->main);
@@ -187,6 +189,7 @@ void enqueue_iteration(jacobi3d* c, int p, bool first, bool last) {
     if (peers) {
         for (int l = 0; l < c->n_local; ++l)
             if (c->has_peer[l]) CK(cudaStreamWaitEvent(c->main, unf ? c->ev_pk[l][q] : c->ev_st[l][q], 0));
+        if (!unf && c->direct_push) copies(c, c->d_push, q, -1, 0, true, c->main);
         cross_gpu_exchange(c, q, q, c->main);
         if (!unf && c->direct_nccl_unpack) copies(c, c->d_unpack_nccl, q, -1, 0, true, c->main);
         CK(cudaEventRecord(c->ev_xw[q], c->main));
@@ -307,6 +310,7 @@ void destroy_ctx(jacobi3d* c) {
     cudaFree(c->d_pack);
     cudaFree(c->d_unpack);
     cudaFree(c->d_unpack_nccl);
+    cudaFree(c->d_push);
     cudaFree(c->d_pack_peer);
     cudaFree(c->d_unpack_peer);
     cudaFree(c->d_pack_local);

@@ -111,7 +111,11 @@ void build_tables(jacobi3d* c) {
                 for (int f = 0; f < 6; ++f) {
                     const int k = c->kind[l][f];
                     if (k == DIRICHLET) continue;
-                    bool direct = v == J3D_FUSE_DIRECT && (k == LOCAL || k == PEER_P2P);
+                    // direct ghost stores: same GPU, or a peer's y/z ghost layer over NVLink.
+                    // Peer x faces (one 8-byte cell per row, scattered NVLink stores cost
+                    // ~10% of the update, profiles/r01_multi_gpu.md) go through the local
+                    // send buffer instead: pushed coalesced to the peer after the update.
+                    bool direct = v == J3D_FUSE_DIRECT && (k == LOCAL || (k == PEER_P2P && f >= 2));
                     if (direct) {
                         const int r = k == LOCAL ? -1 : c->plan.blocks[c->plan.blocks[c->gid[l]].nbr[f]].owner;
                         if (k == PEER_P2P && !c->p2p_connected) continue;  // filled after ipc_connect
@@ -119,11 +123,13 @@ void build_tables(jacobi3d* c) {
                         d.epi_mask |= 1u << f;
                         if (f < 2 && (c->nx % 4) == 0 && c->xsector_ok) d.xsector |= 1u << f;  // whole-sector x-ghost stores
                     } else if (v == J3D_FUSE_DIRECT) {
-                        // NCCL face of the direct variant: epilogue packs into the
-                        // send buffer; after the exchange a batched unpack kernel
-                        // writes the received face into the ghost layer (keeps the
-                        // stencil's prologue empty)
-                        d.epi[f] = pack_dst(c, l, f, q);
+                        // NCCL / host-staged face, or peer x face, of the direct
+                        // variant: the epilogue packs into the local send buffer;
+                        // after the exchange a batched unpack kernel writes the
+                        // received face into the ghost layer (keeps the stencil's
+                        // prologue empty)
+                        if (k == PEER_P2P && !c->p2p_connected) continue;
+                        d.epi[f] = c->contiguous(c->face_buf(l, f, q, false), f);
                         d.epi_mask |= 1u << f;
                     } else {
                         if (k == PEER_P2P && !c->p2p_connected) continue;
@@ -161,16 +167,32 @@ void build_tables(jacobi3d* c) {
             }
     CK(cudaMemcpy(c->d_pack, pack.data(), pack.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->d_unpack, unpack.data(), unpack.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
-    // NCCL faces only (direct variant's post-exchange unpack)
+    // direct variant: faces that travel through the buffers (NCCL, host staging,
+    // peer x faces) -- the push of peer x faces (local send buffer -> the
+    // peer's receive buffer over NVLink, coalesced) and the post-exchange unpack
     c->direct_nccl_unpack = false;
+    c->direct_push = false;
+    std::vector<CopyDesc> push(2 * nl * 6);
     for (int q = 0; q < 2; ++q)
         for (int l = 0; l < nl; ++l)
             for (int f = 0; f < 6; ++f) {
-                CopyDesc& up = unpack[(q * nl + l) * 6 + f];
-                if (!via_buffers(c->kind[l][f])) std::memset(&up, 0, sizeof up);
+                const int i = (q * nl + l) * 6 + f;
+                const int k = c->kind[l][f];
+                CopyDesc& up = unpack[i];
+                std::memset(&push[i], 0, sizeof(CopyDesc));
+                const bool px = k == PEER_P2P && f < 2 && c->p2p_connected;
+                if (!via_buffers(k) && !px) std::memset(&up, 0, sizeof up);
                 else if (v == J3D_FUSE_DIRECT) c->direct_nccl_unpack = true;
+                if (px && v == J3D_FUSE_DIRECT) {
+                    push[i].src = c->contiguous(c->face_buf(l, f, q, false), f);
+                    push[i].dst = pack_dst(c, l, f, q);
+                    push[i].na = (int32_t)c->face_na(f);
+                    push[i].nb = (int32_t)c->face_nb(f);
+                    c->direct_push = true;
+                }
             }
     CK(cudaMemcpy(c->d_unpack_nccl, unpack.data(), unpack.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_push, push.data(), push.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
     // peer-only / local-only tables for the overlap mode
     {
         std::vector<CopyDesc> pk_peer(pack), up_peer(2 * nl * 6), pk_loc(pack), up_loc(2 * nl * 6);
