@@ -169,11 +169,16 @@ __device__ __forceinline__ double sum7(double c, double xm, double xp, double ym
 // Tile shape: TX cells along x (a warp covers 64 with double2 per lane, CPL
 // column groups), NCW consumer warps each owning RPW rows (TY = NCW*RPW),
 // NSTAGE plane buffers in the TMA ring, MINB CTAs per SM targeted.
-template <int TX_, int NCW_, int RPW_, int NSTAGE_, int MINB_>
+template <int TX_, int NCW_, int RPW_, int NSTAGE_, int MINB_, int MAP_ = 0>
 struct Tile {
     static constexpr int TX = TX_, NCW = NCW_, RPW = RPW_, NSTAGE = NSTAGE_, MINB = MINB_;
+    // MAP 0: a lane owns cell pairs (x, x+1), x = x0 + 64c + 2*lane (16-byte accesses);
+    // MAP 1: a lane owns single cells x = x0 + 32k + lane (any TX multiple of 32,
+    //        e.g. a 96-wide block in one tile)
+    static constexpr int MAP = MAP_;
     static constexpr int TY = NCW * RPW;
     static constexpr int CPL = TX / 64;
+    static constexpr int KPL = TX / 32;
     static constexpr int HX = 4;      // halo columns kept left of the tile in smem
     static constexpr int W = TX + 2 * HX;  // smem row: x0-4 .. x0+TX+3: the same 32-B sectors as x0-1 .. x0+TX,
                                            // 16-B aligned interior, rows a multiple of 64 B
@@ -183,7 +188,7 @@ struct Tile {
     static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8 + 2 * 4 * 8 + 4 * 4 + 128;
     static constexpr int THREADS = 32 * (NCW + 1);
     // the consumers hold the stages of planes z-1, z, z+1; at least one more is in flight
-    static_assert(TX % 64 == 0 && W <= 256 && H <= 256 && NSTAGE >= 4, "tile shape");
+    static_assert((MAP == 1 ? TX % 32 : TX % 64) == 0 && W <= 256 && H <= 256 && NSTAGE >= 4, "tile shape");
 };
 
 // Rare path (strategy C prologue, "unpack fused into the update"): overwrite
@@ -386,7 +391,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
         const int nx = d->nx, ny = d->ny, nz = d->nz;
         const int64_t pitch = d->pitch, zs = d->zs;
         const int x0 = w.tx * T::TX, y0 = w.ty * T::TY;
-        const int xl = x0 + 2 * lane, yl = y0 + warp * RPW;  // this thread's first cell (c = 0, r = 0)
+        const int xl = x0 + (T::MAP == 1 ? lane : 2 * lane), yl = y0 + warp * RPW;  // this thread's first cell
         double* obase = d->out + (int64_t)(yl + 1) * pitch + XOFF + xl;
         const uint32_t pro = faces ? d->pro_mask : 0u;
         const uint32_t epi = faces ? d->epi_mask : 0u;
@@ -404,7 +409,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
             if constexpr (HOISTX) return f == 0 ? fxm : fxp;
             else return load_face(&d->epi[f]);
         };
-        const int sbase = (warp * RPW + 1) * W + 2 * lane + T::HX;  // smem offset of cell (r = 0, c = 0)
+        const int sbase = (warp * RPW + 1) * W + (T::MAP == 1 ? lane : 2 * lane) + T::HX;  // smem offset of the first cell
 
         // wait for the stage of plane zz, patch its ghosts (fused prologue) if needed
         auto acquire = [&](int zz) {
@@ -583,6 +588,107 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
             }
         };
 
+        // MAP 1: the same plane update with one cell per lane and column step 32
+        auto compute_plane_s = [&](auto mode_tag, auto whole_tag, int z, uint32_t fm, const double* pm,
+                                   const double* pc, const double* pp) {
+            constexpr int MODE = decltype(mode_tag)::value;
+            constexpr bool WHOLE = decltype(whole_tag)::value;
+            constexpr int KPL = T::KPL;
+            double* op = obase + (int64_t)(z + 1) * zs;
+            double cap0[RPW], cap1[RPW];
+            const int xlast = nx - 1 - x0;
+            const int klast = xlast >> 5, lane_last = xlast & 31;
+            double* zdst = nullptr;
+            int64_t zsb = 0;
+            double* ymd = nullptr;
+            double* ypd = nullptr;
+            uint32_t rare_faces = 0;
+            if constexpr (MODE == 2) {
+                if ((fm & 48u) == 48u) {
+                    rare_faces |= 48u;
+                } else if (fm & 48u) {
+                    const FaceRef F = load_face(&d->epi[(fm & 16u) ? 4 : 5]);
+                    zdst = F.p;
+                    zsb = F.sb;
+                }
+                if (fm & 4u) {
+                    const FaceRef F = load_face(&d->epi[2]);
+                    ymd = F.p + (int64_t)z * F.sb;
+                }
+                if (fm & 8u) {
+                    const FaceRef F = load_face(&d->epi[3]);
+                    ypd = F.p + (int64_t)z * F.sb;
+                }
+            }
+            bool tiny = false;
+#pragma unroll
+            for (int r = 0; r < RPW; ++r) {
+#pragma unroll
+                for (int k = 0; k < KPL; ++k) {
+                    const int off = r * W + 32 * k;
+                    const double* p = pc + off;
+                    const double sv = sum7(p[0], p[-1], p[1], p[-W], p[W], pm[off], pp[off]);
+                    tiny |= fabs(sv) < kDiv7Tiny;
+                    const double v = div7_fast(sv);
+                    if constexpr (MODE >= 1) {
+                        if (k == 0) cap0[r] = v;
+                        if (k == klast) cap1[r] = v;
+                    }
+                    const int x = xl + 32 * k, y = yl + r;
+                    bool v0 = true;
+                    if constexpr (!WHOLE) v0 = y < ny && x < nx;
+                    if (v0) {
+                        double* o = op + r * pitch + 32 * k;
+                        asm volatile("st.global.f64 [%0], %1;" ::"l"(o), "d"(v) : "memory");
+                        if constexpr (MODE == 2) {
+                            if (zdst) zdst[x + (int64_t)y * zsb] = v;
+                            if (ymd && y == 0) ymd[x] = v;
+                            if (ypd && y == ny - 1) ypd[x] = v;
+                        }
+                    }
+                }
+            }
+            if constexpr (MODE >= 1) {  // x faces: the lane owning x = 0 / x = nx-1
+                if ((fm & 1u) && x0 == 0 && lane == 0) {
+                    const FaceRef F = face_x(0);
+                    double* q = F.p + (int64_t)z * F.sb;
+#pragma unroll
+                    for (int r = 0; r < RPW; ++r)
+                        if (yl + r < ny) {
+                            if (d->xsector & 1u) st_ghost_sector(q + (int64_t)(yl + r) * F.sa, cap0[r], false);
+                            else q[(int64_t)(yl + r) * F.sa] = cap0[r];
+                        }
+                }
+                if ((fm & 2u) && klast < KPL && lane == lane_last) {
+                    const FaceRef F = face_x(1);
+                    double* q = F.p + (int64_t)z * F.sb;
+#pragma unroll
+                    for (int r = 0; r < RPW; ++r)
+                        if (yl + r < ny) {
+                            if (d->xsector & 2u) st_ghost_sector(q + (int64_t)(yl + r) * F.sa, cap1[r], true);
+                            else q[(int64_t)(yl + r) * F.sa] = cap1[r];
+                        }
+                }
+            }
+            if (tiny || rare_faces) {
+#pragma unroll
+                for (int r = 0; r < RPW; ++r) {
+#pragma unroll
+                    for (int k = 0; k < KPL; ++k) {
+                        const int x = xl + 32 * k, y = yl + r;
+                        if (y >= ny || x >= nx) continue;
+                        const int off = r * W + 32 * k;
+                        const double* p = pc + off;
+                        const double v = div7(sum7(p[0], p[-1], p[1], p[-W], p[W], pm[off], pp[off]));
+                        op[r * pitch + 32 * k] = v;
+                        const uint32_t m = tiny ? fm : (rare_faces & fm);
+                        // epi_store writes pairs; pass (v, v) with has2 = false
+                        if (m) epi_store(d, m, x, y, z, v, v, false);
+                    }
+                }
+            }
+        };
+
         // stages of planes z-1, z, z+1 are held; every value is read from smem
         acquire(w.z0 - 1);
         int sm = s;
@@ -601,10 +707,17 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
             using M0 = std::integral_constant<int, 0>;
             using M1 = std::integral_constant<int, 1>;
             using M2 = std::integral_constant<int, 2>;
-            if (fm & ~3u) compute_plane(M2{}, std::false_type{}, z, fm, pm, pc, pp);
-            else if (fm) compute_plane(M1{}, std::false_type{}, z, fm, pm, pc, pp);
-            else if (whole) compute_plane(M0{}, std::true_type{}, z, 0u, pm, pc, pp);
-            else compute_plane(M0{}, std::false_type{}, z, 0u, pm, pc, pp);
+            if constexpr (T::MAP == 1) {
+                if (fm & ~3u) compute_plane_s(M2{}, std::false_type{}, z, fm, pm, pc, pp);
+                else if (fm) compute_plane_s(M1{}, std::false_type{}, z, fm, pm, pc, pp);
+                else if (whole) compute_plane_s(M0{}, std::true_type{}, z, 0u, pm, pc, pp);
+                else compute_plane_s(M0{}, std::false_type{}, z, 0u, pm, pc, pp);
+            } else {
+                if (fm & ~3u) compute_plane(M2{}, std::false_type{}, z, fm, pm, pc, pp);
+                else if (fm) compute_plane(M1{}, std::false_type{}, z, fm, pm, pc, pp);
+                else if (whole) compute_plane(M0{}, std::true_type{}, z, 0u, pm, pc, pp);
+                else compute_plane(M0{}, std::false_type{}, z, 0u, pm, pc, pp);
+            }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[sm]);
             sm = sc;
@@ -755,7 +868,14 @@ cudaError_t launch_div7_selftest(uint64_t n, uint64_t seed, unsigned long long* 
     X(8, 128, 15, 2, 6, 1)  /* 128x30, 6 stages                          */ \
     X(9, 64, 6, 2, 6, 2)    /* 64x12, 2 CTAs/SM (7 warps)                */ \
     X(10, 64, 12, 2, 6, 1)  /* 64x24, 1 CTA/SM                           */ \
-    X(11, 64, 7, 2, 6, 2)   /* 64x14, 2 CTAs/SM (8 warps)                */
+    X(11, 64, 7, 2, 6, 2)   /* 64x14, 2 CTAs/SM (8 warps)                */ \
+    X(12, -96, 8, 2, 6, 2)  /* 96x16 one cell per lane (96-wide blocks)  */ \
+    X(13, -96, 16, 2, 4, 1) /* 96x32 one cell per lane                   */ \
+    X(14, -96, 8, 1, 8, 2)  /* 96x8 one cell per lane                    */ \
+    X(15, -96, 8, 1, 6, 3)  /* 96x8, 3 CTAs/SM                           */ \
+    X(16, -96, 12, 1, 8, 2) /* 96x12                                     */ \
+    X(17, -192, 11, 2, 5, 1) /* 192x22 one cell per lane                 */ \
+    X(18, -96, 6, 2, 8, 2)  /* 96x12 (RPW 2)                             */
 
 template <class T>
 static cudaError_t launch_t(const StencilLaunch& L, cudaStream_t st) {
@@ -781,14 +901,14 @@ static cudaError_t occ_t(int* blocks) {
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, stencil_tma_kernel<T>, T::THREADS, T::SMEM_BYTES);
 }
 
-#define J3D_TYPE(k, tx, ncw, rpw, ns, mb) Tile<tx, ncw, rpw, ns, mb>
+#define J3D_TYPE(k, tx, ncw, rpw, ns, mb) Tile<(tx > 0 ? tx : -tx), ncw, rpw, ns, mb, (tx > 0 ? 0 : 1)>
 
-int num_tile_kinds() { return 12; }
+int num_tile_kinds() { return 19; }
 
 TileShape tile_shape(int kind) {
     switch (kind) {
 #define X(k, tx, ncw, rpw, ns, mb) \
-    case k: return TileShape{tx, ncw * rpw};
+    case k: return TileShape{(tx > 0 ? tx : -tx), ncw * rpw};
         J3D_TILES(X)
 #undef X
     }

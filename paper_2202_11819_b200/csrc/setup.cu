@@ -230,14 +230,15 @@ void build_static_tables(jacobi3d* c) {
     // ---- tensor maps [2*l + p] over each input buffer
     g_drv.load();
     // 192x22 tiles (11 consumer warps, 5-stage ring, 1 CTA/SM) when they divide
-    // the block width, else 128x30 (15 consumer warps) for wide blocks and
-    // 64x16 (2 CTAs/SM, 6 stages) for narrow ones.  Bench sweeps: profiles/.
-    c->tile_kind = (c->nx % 192 == 0) ? 0 : c->nx >= 128 ? 1 : 4;
-    {  // small grids: the wide tiles cannot keep every SM busy -> 64x16, 2 CTAs/SM
+    // the block width, else 128x30 (15 consumer warps) for wide blocks, 96x8
+    // one-cell-per-lane tiles for 96-wide blocks (BASELINE configs[4]) and
+    // 64x16 (2 CTAs/SM, 6 stages) for other narrow ones.  Sweeps: profiles/.
+    c->tile_kind = (c->nx % 192 == 0) ? 0 : c->nx >= 128 ? 1 : (c->nx == 96) ? 14 : 4;
+    if (c->tile_kind <= 1) {  // small grids: the wide tiles cannot keep every SM busy -> 64x16, 2 CTAs/SM
         const TileShape t = tile_shape(c->tile_kind);
         const int64_t tiles = ((c->nx + t.tx - 1) / t.tx) * ((c->ny + t.ty - 1) / t.ty) * nl;
         const int64_t max_items = tiles * std::max<int64_t>(1, c->nz / 24);
-        if (c->tile_kind != 4 && max_items < 4LL * c->sms) c->tile_kind = 4;
+        if (max_items < 4LL * c->sms) c->tile_kind = 4;
     }
     if (const char* e = std::getenv("J3D_TILE")) {  // tuning override (bench sweeps)
         const int k = std::atoi(e);

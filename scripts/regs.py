@@ -11,8 +11,8 @@ for line in out.splitlines():
     m = re.search(r"Compiling entry function '(\S+)'", line)
     if m:
         name = m.group(1)
-        t = re.search(r"TileILi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)E", name)
-        cur = f"TX={t.group(1)} NCW={t.group(2)} RPW={t.group(3)} NS={t.group(4)} MINB={t.group(5)}" if t else name[:40]
+        t = re.search(r"TileILi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)E", name)
+        cur = f"TX={t.group(1)} NCW={t.group(2)} RPW={t.group(3)} NS={t.group(4)} MINB={t.group(5)} MAP={t.group(6)}" if t else name[:40]
         continue
     m = re.search(r"(\d+) bytes stack frame, (\d+) bytes spill stores, (\d+) bytes spill loads", line)
     if m and cur:
