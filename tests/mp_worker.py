@@ -124,6 +124,51 @@ def run_set_block_case(grid, odf, variant, exchange):
         ctx.close()
 
 
+def run_api_case(grid):
+    """Rank-local API errors and the epoch-wait watchdog on a multi-GPU context:
+    get_block of a block owned by another rank -> J3D_ENOTLOCAL; a rank whose
+    peer is late surfaces J3D_ETIMEOUT from synchronize (J3D_TIMEOUT_S) and
+    completes once the peer catches up."""
+    import time
+    import paper_2202_11819_b200 as j3d
+    from paper_2202_11819_b200 import jacobi3d as jb
+
+    rank = dist.get_rank()
+    ctx = jdist.create(grid, odf=2, variant="direct", exchange="p2p")
+    try:
+        ctx.init("hash", seed=1)
+        other = [b for b in range(ctx.n_blocks) if ctx.block_info(b)[2] != rank][0]
+        try:
+            ctx.get_block(other)
+            raise AssertionError("get_block of a remote block must fail")
+        except j3d.Jacobi3DError as e:
+            assert e.code == jb.ENOTLOCAL, e
+        dist.barrier()
+        os.environ["J3D_TIMEOUT_S"] = "3"
+        if rank == 0:
+            ctx.iterate(2)
+            try:
+                ctx.synchronize()
+                raise AssertionError("synchronize must time out while the peer is late")
+            except j3d.Jacobi3DError as e:
+                assert e.code == jb.ETIMEOUT, e
+            os.environ["J3D_TIMEOUT_S"] = "600"
+            ctx.synchronize()  # completes once rank 1 has iterated too
+        else:
+            time.sleep(8)
+            os.environ["J3D_TIMEOUT_S"] = "600"
+            ctx.iterate(2)
+            ctx.synchronize()
+        os.environ["J3D_TIMEOUT_S"] = "600"
+        dist.barrier()
+        got = ctx.gather_local()
+        want = core.owned(core.run(core.init(*grid, core.INIT_HASH, seed=1), 2))
+        mask = ~np.isnan(got)
+        assert (got.view(np.uint64)[mask] == np.ascontiguousarray(want).view(np.uint64)[mask]).all()
+    finally:
+        ctx.close()
+
+
 def main():
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
@@ -168,6 +213,12 @@ def main():
         cases += [((16, 8, 16), 1, v, "batched", False, "host", 2, "hash", 3) for v in ("unfused", "direct")]
     n, failed = 0, []
     if which != "debug":
+        try:
+            run_api_case(g)
+        except AssertionError as e:
+            failed.append(str(e))
+            print("FAIL", e, flush=True)
+        n += 1
         for v, x in (("direct", "p2p"), ("unfused", "nccl"), ("C", "host")):
             try:
                 run_set_block_case(g, 2, v, x)

@@ -31,7 +31,7 @@ def test_multi_gpu_parity():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(ROOT, "tests", "mp_worker.py"), os.environ.get("J3D_MP_CASES", "quick")]
-    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=1800, cwd=ROOT)
     assert p.returncode == 0 and "MP OK" in p.stdout, p.stdout[-3000:] + p.stderr[-5000:]
 
 
