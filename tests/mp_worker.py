@@ -189,6 +189,9 @@ def main():
     gx = (96, 48, 48) if world >= 4 else (96, 40, 40)
     for exchange, variant in itertools.product(["p2p", "nccl"], ["direct", "C", "unfused"]):
         cases.append((gx, 2, variant, "batched", False, exchange, 6, "hash", 5))
+    for graph in (False, True):  # peer x faces pushed after the update, per-block streams
+        cases.append((gx, 2, "direct", "per_block", graph, "p2p", 6, "hash", 5))
+        cases.append((gx, 2, "direct", "batched", graph, "p2p", 6, "hash", 5, True))
     # exterior-first overlap (BATCHED), with and without graphs, every variant and backend
     for exchange, variant, graph in itertools.product(["p2p", "nccl"], ["direct", "C", "unfused", "A"],
                                                       [False, True]):
