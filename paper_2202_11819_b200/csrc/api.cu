@@ -148,6 +148,8 @@ int jacobi3d_create(const jacobi3d_config* cfg, const uint8_t* nccl_uid, jacobi3
         CK(cudaMalloc(&c->d_sched, sizeof(unsigned int) * 2 * (c->n_local + 1)));
         CK(cudaMemset(c->d_sched, 0, sizeof(unsigned int) * 2 * (c->n_local + 1)));
         if (const char* e = std::getenv("J3D_XSECTOR")) c->xsector_ok = std::atoi(e) != 0;
+        if (const char* e = std::getenv("J3D_PEERX_DIRECT")) c->peer_x_direct = std::atoi(e) != 0;
+        if (const char* e = std::getenv("J3D_PEERX_PACK")) c->peer_x_pack = std::atoi(e) != 0;
         c->peer_base.assign(c->n_gpus, nullptr);
         build_static_tables(c);
         build_tables(c);

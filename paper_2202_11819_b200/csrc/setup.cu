@@ -113,15 +113,18 @@ void build_tables(jacobi3d* c) {
                     if (k == DIRICHLET) continue;
                     // direct ghost stores: same GPU, or a peer's y/z ghost layer over NVLink.
                     // Peer x faces (one 8-byte cell per row, scattered NVLink stores cost
-                    // ~10% of the update, profiles/r01_multi_gpu.md) go through the local
-                    // send buffer instead: pushed coalesced to the peer after the update.
-                    bool direct = v == J3D_FUSE_DIRECT && (k == LOCAL || (k == PEER_P2P && f >= 2));
+                    // ~10% of the update, profiles/r01_multi_gpu.md) are instead packed
+                    // from the output after the update and pushed to the peer's receive
+                    // buffer (capturing them in the epilogue cost the update 1.7%).
+                    bool direct = v == J3D_FUSE_DIRECT && (k == LOCAL || (k == PEER_P2P && (f >= 2 || c->peer_x_direct)));
                     if (direct) {
                         const int r = k == LOCAL ? -1 : c->plan.blocks[c->plan.blocks[c->gid[l]].nbr[f]].owner;
                         if (k == PEER_P2P && !c->p2p_connected) continue;  // filled after ipc_connect
                         d.epi[f] = c->layer(c->buf(c->nbr_local[l][f], q, r), f ^ 1, true);
                         d.epi_mask |= 1u << f;
                         if (f < 2 && (c->nx % 4) == 0 && c->xsector_ok) d.xsector |= 1u << f;  // whole-sector x-ghost stores
+                    } else if (v == J3D_FUSE_DIRECT && f < 2 && c->peer_x_pack) {
+                        continue;  // peer x face: packed from the output by the push kernel
                     } else if (v == J3D_FUSE_DIRECT) {
                         // NCCL / host-staged face, or peer x face, of the direct
                         // variant: the epilogue packs into the local send buffer;
@@ -180,11 +183,14 @@ void build_tables(jacobi3d* c) {
                 const int k = c->kind[l][f];
                 CopyDesc& up = unpack[i];
                 std::memset(&push[i], 0, sizeof(CopyDesc));
-                const bool px = k == PEER_P2P && f < 2 && c->p2p_connected;
+                const bool px = k == PEER_P2P && f < 2 && c->p2p_connected && !c->peer_x_direct;
                 if (!via_buffers(k) && !px) std::memset(&up, 0, sizeof up);
                 else if (v == J3D_FUSE_DIRECT) c->direct_nccl_unpack = true;
-                if (px && v == J3D_FUSE_DIRECT) {
-                    push[i].src = c->contiguous(c->face_buf(l, f, q, false), f);
+                // x faces that leave through buffers: pushed from the output (peer_x_pack)
+                // or from the send buffer the epilogue filled (P2P only)
+                if (v == J3D_FUSE_DIRECT && f < 2 && (px || (via_buffers(k) && c->peer_x_pack))) {
+                    push[i].src = c->peer_x_pack ? c->layer(c->buf(l, q), f, false)
+                                                 : c->contiguous(c->face_buf(l, f, q, false), f);
                     push[i].dst = pack_dst(c, l, f, q);
                     push[i].na = (int32_t)c->face_na(f);
                     push[i].nb = (int32_t)c->face_nb(f);
