@@ -74,6 +74,15 @@ extern "C" {
 #define J3D_PER_BLOCK    0  /* one launch per block; per-block prioritised streams: update on a
                                low-priority stream, (un)pack on a high-priority stream         */
 #define J3D_BATCHED      1  /* one launch per kernel kind per GPU covering all its blocks       */
+#define J3D_PERSISTENT   2  /* one launch per jacobi3d_iterate(n) call performing all n
+                               iterations: the persistent grid walks n x (work items) in order
+                               and an item of iteration k+1 starts as soon as the z-chunk slabs
+                               it reads (own block and neighbour blocks) finished iteration k,
+                               tracked by on-device completion counters -- no launch, no
+                               host sync and no grid-wide tail between iterations (PAPER.md
+                               L739-749: launch/sync overhead at fine granularity).  Requires
+                               variant J3D_FUSE_DIRECT, n_gpus == 1, use_graph == 0, else
+                               J3D_EINVAL                                                      */
 
 /* ---- exchange backend between GPUs (same-GPU faces are always LOCAL) ---- */
 #define J3D_XCHG_AUTO    0  /* P2P when every peer is reachable over NVLink, else NCCL          */
@@ -101,7 +110,7 @@ typedef struct {
     int32_t rank;         /* this process's rank in [0, n_gpus)                                  */
     int32_t device;       /* CUDA device ordinal this rank uses                                  */
     int32_t variant;      /* J3D_UNFUSED .. J3D_FUSE_DIRECT                                      */
-    int32_t launch;       /* J3D_PER_BLOCK | J3D_BATCHED                                          */
+    int32_t launch;       /* J3D_PER_BLOCK | J3D_BATCHED | J3D_PERSISTENT                         */
     int32_t use_graph;    /* 1: capture one iteration per buffer parity into two CUDA graphs and
                              alternate them; 0: direct launches             */
     int32_t exchange;     /* J3D_XCHG_*                                                          */

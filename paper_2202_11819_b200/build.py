@@ -16,7 +16,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
-LIB = os.path.join(HERE, "libjacobi3d.so")
+LIB = os.path.join(HERE, os.environ.get("J3D_LIB_OUT", "libjacobi3d.so"))  # J3D_LIB_OUT: experiment builds
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -55,12 +55,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     inc, libdir = nccl_dirs()
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build" if LIB.endswith("libjacobi3d.so") else "build_" + os.path.basename(LIB))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-I", inc, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        defs = [f"-DJ3D_XOFF={os.environ['J3D_XOFF']}"] if os.environ.get("J3D_XOFF") else []
+        cmd = [NVCC, *ARCH, *FLAGS, *defs, "-I", inc, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), flush=True)

@@ -35,7 +35,10 @@ int guarded(F&& f) {
 int validate_cfg(const jacobi3d_config* c) {
     if (!c) return fail(J3D_EINVAL, "config is NULL");
     if (c->variant < J3D_UNFUSED || c->variant > J3D_FUSE_DIRECT) return fail(J3D_EINVAL, "unknown variant");
-    if (c->launch != J3D_PER_BLOCK && c->launch != J3D_BATCHED) return fail(J3D_EINVAL, "unknown launch mode");
+    if (c->launch != J3D_PER_BLOCK && c->launch != J3D_BATCHED && c->launch != J3D_PERSISTENT)
+        return fail(J3D_EINVAL, "unknown launch mode");
+    if (c->launch == J3D_PERSISTENT && (c->variant != J3D_FUSE_DIRECT || c->n_gpus != 1 || c->use_graph != 0))
+        return fail(J3D_EINVAL, "J3D_PERSISTENT needs variant J3D_FUSE_DIRECT, n_gpus == 1 and use_graph == 0");
     if (c->exchange < J3D_XCHG_AUTO || c->exchange > J3D_XCHG_HOST) return fail(J3D_EINVAL, "unknown exchange backend");
     if (c->n_gpus < 1 || c->rank < 0 || c->rank >= c->n_gpus) return fail(J3D_EINVAL, "rank / n_gpus out of range");
     if (c->odf < 1) return fail(J3D_EINVAL, "odf must be >= 1");

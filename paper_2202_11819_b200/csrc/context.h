@@ -176,6 +176,14 @@ struct jacobi3d {
     std::vector<int> item_begin, item_count;  // per local block, in d_items
     std::vector<int64_t> item_cells;          // prefix sums of owned cells per item (profiling bytes)
     int n_items = 0, tile_kind = 0, grid_cap = 0;
+    // J3D_PERSISTENT: slab dependency tables and completion counters (device.cuh IterCtl)
+    int32_t* d_item_slab = nullptr;             // [n_items]
+    int32_t* d_slab_deps = nullptr;             // [n_slabs][MAX_DEPS]
+    unsigned int* d_done = nullptr;             // [n_slabs]
+    int n_slabs = 0;
+    uint32_t slab_target = 0;                   // consumer warps x tiles per slab
+    uint32_t persist_base = 0;                  // iterations counted in d_done (mod 2^32)
+    int persist_n = 0;                          // set while launching a persistent stencil
     bool faces_fused = false;                   // stencil launches carry prologue/epilogue faces
     std::vector<int> order;                     // local blocks, peer-face blocks first
 

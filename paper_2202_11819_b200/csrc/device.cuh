@@ -14,7 +14,10 @@
 
 namespace j3d {
 
-constexpr int XOFF = 16;
+#ifndef J3D_XOFF
+#define J3D_XOFF 16
+#endif
+constexpr int XOFF = J3D_XOFF;  // even (16-byte aligned cell pairs); -DJ3D_XOFF only for layout experiments
 constexpr int PITCH_ALIGN = 16;  // doubles
 
 struct FaceRef {  // element (a,b) of a 2D face lives at p[a*sa + b*sb]
@@ -42,6 +45,25 @@ struct WorkItem {
     int32_t blk;    // local block index (descriptor = 2*blk + parity)
     int16_t tx, ty; // tile coordinates
     int32_t z0, z1;
+};
+
+// Multi-iteration (persistent) stencil launches, J3D_PERSISTENT: launch item g
+// is item (g mod n_items) of relative iteration k = g / n_items.  A slab is
+// one block's tiles over one z chunk; done[s] counts consumer-warp completions
+// of slab s (mod 2^32, never reset).  An item of iteration k > 0 may start
+// once every slab in slab_deps[item_slab[i]] -- the slabs whose iteration-k-1
+// writes it reads (its own and the adjacent z chunks, the x/y neighbour
+// blocks' same chunk, the z neighbour's edge chunk) and, by symmetry, those
+// whose iteration-k-1 reads its writes would clobber -- has
+// done >= (base + k) * target.
+constexpr int MAX_DEPS = 9;
+struct IterCtl {
+    const int32_t* item_slab;  // [n_items]
+    const int32_t* slab_deps;  // [n_slabs][MAX_DEPS], -1 padded
+    unsigned int* done;        // [n_slabs]; nullptr: one iteration, no tracking
+    int32_t n_iter;            // iterations in this launch
+    uint32_t target;           // completions per slab per iteration (consumer warps x tiles per slab)
+    uint32_t base;             // iterations counted in done[] before this launch
 };
 
 // A strided 2D face copy (pack: owned layer -> send buffer / peer receive

@@ -62,6 +62,37 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ uint32_t ld_acquire_u32(const unsigned int* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Persistent launches: wait until the slabs item `it` depends on have
+// finished `iters` iterations (IterCtl, device.cuh), then order the async
+// proxy (TMA) after the acquired generic-proxy writes.  A wait beyond 60 s
+// can only be a bug: trap rather than hang the GPU.
+__device__ __noinline__ void wait_slabs(const IterCtl ctl, int it, uint32_t iters) {
+    const uint32_t need = iters * ctl.target;
+    const int32_t* dp = ctl.slab_deps + (int64_t)ctl.item_slab[it] * MAX_DEPS;
+    for (int j = 0; j < MAX_DEPS; ++j) {
+        const int t = dp[j];
+        if (t < 0) break;
+        if ((int32_t)(ld_acquire_u32(ctl.done + t) - need) >= 0) continue;
+        const uint64_t t0 = global_ns();
+        while ((int32_t)(ld_acquire_u32(ctl.done + t) - need) < 0) {
+            __nanosleep(128);
+            if (global_ns() - t0 > 60ull * 1000000000ull) __trap();
+        }
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 __device__ __forceinline__ void tmap_acquire(const CUtensorMap* m) {
     asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(reinterpret_cast<uint64_t>(m))
                  : "memory");
@@ -296,7 +327,7 @@ template <class T>
 __global__ void __launch_bounds__(T::THREADS, T::MINB)
     stencil_tma_kernel(const StencilDesc* __restrict__ descs, const CUtensorMap* __restrict__ tmaps,
                        const CUtensorMap* __restrict__ tmaps3, const WorkItem* __restrict__ items, int n_items,
-                       int parity, int flags, unsigned int* __restrict__ sched) {
+                       int parity, int flags, unsigned int* __restrict__ sched, const IterCtl ctl) {
     constexpr int NCW = T::NCW, RPW = T::RPW, CPL = T::CPL, W = T::W, NSTAGE = T::NSTAGE, IQ = 4;
     // The kernel has no static shared memory, so the dynamic window starts at
     // shared offset 0 (1024-B aligned); indexing the __shared__ array directly
@@ -331,16 +362,19 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
             uint64_t pol_first = 0, pol_last = 0;
             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
             asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
+            const int total = n_items * ctl.n_iter;
             for (;;) {
-                int it = (int)atomicAdd(&sched[0], 1u);
-                if (it >= n_items) it = -1;
+                int g = (int)atomicAdd(&sched[0], 1u);
+                if (g >= total) g = -1;
                 mbar_wait(&qempty[qs], qph ^ 1);
-                queue[qs] = it;
+                queue[qs] = g;
                 mbar_arrive(&qfull[qs]);
                 if (++qs == IQ) { qs = 0; qph ^= 1; }
-                if (it < 0) break;
+                if (g < 0) break;
+                const int k = g / n_items, it = g - k * n_items;
                 const WorkItem w = items[it];
-                const CUtensorMap* tm = tmaps + (2 * w.blk + parity);
+                if (k > 0) wait_slabs(ctl, it, ctl.base + (uint32_t)k);
+                const CUtensorMap* tm = tmaps + (2 * w.blk + (parity ^ (k & 1)));
                 tmap_acquire(tm);
                 const int c0 = XOFF + w.tx * T::TX - T::HX, c1 = w.ty * T::TY;
                 for (int z = w.z0 - 1; z <= w.z1; ++z) {
@@ -354,7 +388,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                     } else {
                         // the two rows at each end of the box are shared with the
                         // y-neighbour tiles: keep them (evict_last); stream the rest
-                        const CUtensorMap* t2 = tmaps3 + 2 * (2 * w.blk + parity);
+                        const CUtensorMap* t2 = tmaps3 + 2 * (2 * w.blk + (parity ^ (k & 1)));
                         tma_load_3d_hint(dst, t2, &full[s], c0, c1, z + 1, pol_last);
                         tma_load_3d_hint(dst + 2 * T::W * 8, t2 + 1, &full[s], c0, c1 + 2, z + 1, pol_first);
                         tma_load_3d_hint(dst + (T::H - 2) * T::W * 8, t2, &full[s], c0, c1 + T::H - 2, z + 1, pol_last);
@@ -380,14 +414,15 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
 
     for (;;) {
         mbar_wait(&qfull[qs], qph);
-        const int it = queue[qs];
+        const int g = queue[qs];
         __syncwarp();
         if (lane == 0) mbar_arrive(&qempty[qs]);
         if (++qs == IQ) { qs = 0; qph ^= 1; }
-        if (it < 0) break;
+        if (g < 0) break;
+        const int kit = g / n_items, it = g - kit * n_items;
 
         const WorkItem w = items[it];
-        const StencilDesc* d = descs + (2 * w.blk + parity);
+        const StencilDesc* d = descs + (2 * w.blk + (parity ^ (kit & 1)));
         const int nx = d->nx, ny = d->ny, nz = d->nz;
         const int64_t pitch = d->pitch, zs = d->zs;
         const int x0 = w.tx * T::TX, y0 = w.ty * T::TY;
@@ -728,6 +763,11 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
             mbar_arrive(&empty[sm]);  // plane z1-1
             mbar_arrive(&empty[sc]);  // plane z1
         }
+        if (ctl.done) {  // persistent launch: publish this warp's part of the item (release)
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) atomicAdd(ctl.done + ctl.item_slab[it], 1u);
+        }
     }
 }
 
@@ -889,7 +929,7 @@ static cudaError_t launch_t(const StencilLaunch& L, cudaStream_t st) {
     if (L.n_items <= 0) return cudaSuccess;
     stencil_tma_kernel<T><<<L.grid, T::THREADS, T::SMEM_BYTES, st>>>(
         L.descs, L.tmaps, L.tmaps_split, L.items, L.n_items, L.parity,
-        (L.faces ? 1 : 0) | ((L.tma_mode & 3) << 2), L.sched);
+        (L.faces ? 1 : 0) | ((L.tma_mode & 3) << 2), L.sched, L.ctl);
     return cudaGetLastError();
 }
 
@@ -908,11 +948,11 @@ int num_tile_kinds() { return 19; }
 TileShape tile_shape(int kind) {
     switch (kind) {
 #define X(k, tx, ncw, rpw, ns, mb) \
-    case k: return TileShape{(tx > 0 ? tx : -tx), ncw * rpw};
+    case k: return TileShape{(tx > 0 ? tx : -tx), ncw * rpw, ncw};
         J3D_TILES(X)
 #undef X
     }
-    return TileShape{0, 0};
+    return TileShape{0, 0, 0};
 }
 
 cudaError_t launch_stencil(const StencilLaunch& L, cudaStream_t st) {

@@ -11,6 +11,7 @@ namespace j3d {
 
 struct TileShape {
     int tx, ty;
+    int ncw;  // consumer warps per CTA
 };
 
 struct StencilLaunch {
@@ -25,6 +26,7 @@ struct StencilLaunch {
     int kind;    // tile configuration (kernels.cu J3D_TILES)
     bool faces;  // any prologue/epilogue faces in this launch
     unsigned int* sched;     // device [2] scheduler counters (zero on entry; reset by the kernel)
+    IterCtl ctl;             // iterations in this launch + slab dependency tracking (persistent)
 };
 
 int num_tile_kinds();

@@ -41,6 +41,12 @@ void stencil(jacobi3d* c, int begin, int count, int parity, cudaStream_t st, int
     L.kind = c->tile_kind;
     L.faces = c->faces_fused;
     L.sched = c->d_sched + 2 * (l + 1);  // one counter pair per concurrently running launch
+    L.ctl = IterCtl{nullptr, nullptr, nullptr, 1, 0, 0};
+    const int n_iter = c->persist_n;
+    if (n_iter > 0) {  // J3D_PERSISTENT: n_iter iterations in this one launch
+        L.ctl = IterCtl{c->d_item_slab, c->d_slab_deps, c->d_done, n_iter, c->slab_target, c->persist_base};
+        L.grid = c->grid_cap;
+    }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     const bool prof = c->prof && !c->capturing;
     if (prof) {
@@ -54,7 +60,7 @@ void stencil(jacobi3d* c, int begin, int count, int parity, cudaStream_t st, int
         CK(cudaEventRecord(e1, st));
         c->prof_events.push_back({e0, e1});
         const int64_t cells = c->item_cells[begin + count] - c->item_cells[begin];  // exact owned cells updated
-        c->prof_pending_bytes += 16.0 * (double)cells;
+        c->prof_pending_bytes += 16.0 * (double)cells * (double)std::max(1, n_iter);
     }
 }
 
@@ -258,6 +264,22 @@ void do_iterate(jacobi3d* c, int64_t n) {
     }
     if (c->p2p_needed && !c->p2p_connected)
         throw Error(J3D_ESTATE, "P2P exchange needs jacobi3d_ipc_export/jacobi3d_ipc_connect first");
+    if (c->cfg.launch == J3D_PERSISTENT) {
+        // one launch per call (split only to keep n x items inside the 32-bit work counter)
+        const int64_t cap = std::max<int64_t>(1, std::min<int64_t>(1 << 20, INT32_MAX / std::max(1, c->n_items)));
+        for (int64_t left = n; left > 0;) {
+            const int m = (int)std::min(left, cap);
+            c->persist_n = m;
+            stencil(c, 0, c->n_items, (int)(c->iter & 1), c->main, -1);
+            c->persist_n = 0;
+            c->persist_base += (uint32_t)m;
+            c->iter += m;
+            c->iter_since_set += m;
+            c->stat_iters += m;
+            left -= m;
+        }
+        return;
+    }
     for (int64_t k = 0; k < n; ++k) {
         const int p = (int)(c->iter & 1);
         if (c->cfg.use_graph) {
@@ -311,6 +333,9 @@ void destroy_ctx(jacobi3d* c) {
     cudaFree(c->d_unpack);
     cudaFree(c->d_unpack_nccl);
     cudaFree(c->d_push);
+    cudaFree(c->d_item_slab);
+    cudaFree(c->d_slab_deps);
+    cudaFree(c->d_done);
     cudaFree(c->d_pack_peer);
     cudaFree(c->d_unpack_peer);
     cudaFree(c->d_pack_local);

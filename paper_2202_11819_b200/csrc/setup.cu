@@ -122,7 +122,7 @@ void build_tables(jacobi3d* c) {
                         if (k == PEER_P2P && !c->p2p_connected) continue;  // filled after ipc_connect
                         d.epi[f] = c->layer(c->buf(c->nbr_local[l][f], q, r), f ^ 1, true);
                         d.epi_mask |= 1u << f;
-                        if (f < 2 && (c->nx % 4) == 0 && c->xsector_ok) d.xsector |= 1u << f;  // whole-sector x-ghost stores
+                        if (f < 2 && (c->nx % 4) == 0 && XOFF % 4 == 0 && c->xsector_ok) d.xsector |= 1u << f;  // whole-sector x-ghost stores
                     } else if (v == J3D_FUSE_DIRECT && f < 2 && c->peer_x_pack) {
                         continue;  // peer x face: packed from the output by the push kernel
                     } else if (v == J3D_FUSE_DIRECT) {
@@ -354,6 +354,40 @@ void build_static_tables(jacobi3d* c) {
         const int64_t ex = std::min<int64_t>(ts.tx, c->nx - (int64_t)w.tx * ts.tx);
         const int64_t ey = std::min<int64_t>(ts.ty, c->ny - (int64_t)w.ty * ts.ty);
         c->item_cells[i + 1] = c->item_cells[i] + ex * ey * (w.z1 - w.z0);
+    }
+    if (c->cfg.launch == J3D_PERSISTENT) {
+        // slab = (local block, z chunk); deps of a slab (IterCtl, device.cuh): its own and the
+        // adjacent z chunks of the block, the same chunk of the x/y neighbour blocks, and for
+        // an edge chunk the z neighbour's edge chunk it exchanges a ghost plane with
+        const int nzc = (int)best_zc;
+        c->n_slabs = nl * nzc;
+        c->slab_target = (uint32_t)(ts.ncw * ntx * nty);
+        std::vector<int32_t> slab(items.size()), deps((size_t)c->n_slabs * MAX_DEPS, -1);
+        for (size_t i = 0; i < items.size(); ++i) {
+            const WorkItem& w = items[i];
+            int zc = 0;
+            while ((int)(c->nz * (zc + 1) / best_zc) <= w.z0) ++zc;
+            slab[i] = w.blk * nzc + zc;
+        }
+        for (int l = 0; l < nl; ++l)
+            for (int zc = 0; zc < nzc; ++zc) {
+                int32_t* d = &deps[(size_t)(l * nzc + zc) * MAX_DEPS];
+                int n = 0;
+                for (int dz = -1; dz <= 1; ++dz)
+                    if (zc + dz >= 0 && zc + dz < nzc) d[n++] = l * nzc + zc + dz;
+                for (int f = 0; f < 4; ++f)
+                    if (c->kind[l][f] == LOCAL) d[n++] = c->nbr_local[l][f] * nzc + zc;
+                if (zc == 0 && c->kind[l][4] == LOCAL) d[n++] = c->nbr_local[l][4] * nzc + (nzc - 1);
+                if (zc == nzc - 1 && c->kind[l][5] == LOCAL) d[n++] = c->nbr_local[l][5] * nzc;
+                if (n > MAX_DEPS) throw Error(J3D_EUNSUPPORTED, "slab dependency table overflow");
+            }
+        CK(cudaMalloc(&c->d_item_slab, std::max<size_t>(1, slab.size()) * sizeof(int32_t)));
+        CK(cudaMemcpy(c->d_item_slab, slab.data(), slab.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        CK(cudaMalloc(&c->d_slab_deps, deps.size() * sizeof(int32_t)));
+        CK(cudaMemcpy(c->d_slab_deps, deps.data(), deps.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        CK(cudaMalloc(&c->d_done, (size_t)c->n_slabs * sizeof(unsigned int)));
+        CK(cudaMemset(c->d_done, 0, (size_t)c->n_slabs * sizeof(unsigned int)));
+        c->persist_base = 0;
     }
     CK(cudaMalloc(&c->d_items, std::max<size_t>(1, items.size()) * sizeof(WorkItem)));
     CK(cudaMemcpy(c->d_items, items.data(), items.size() * sizeof(WorkItem), cudaMemcpyHostToDevice));

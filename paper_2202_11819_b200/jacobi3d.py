@@ -12,15 +12,15 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libjacobi3d.so")
+LIB_PATH = os.path.join(_HERE, os.environ.get("J3D_LIB", "libjacobi3d.so"))  # J3D_LIB: experiment builds
 
 # status codes
 OK, EINVAL, EDECOMP, ENOMEM, ECUDA, ENCCL, ENOTLOCAL, ESTATE, ETIMEOUT, EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6, -7, -8, -9
 # variants (PAPER.md L515-521 strategies A/B/C + the direct-ghost B200 variant)
 UNFUSED, FUSE_A, FUSE_B, FUSE_C, FUSE_DIRECT = 0, 1, 2, 3, 4
 VARIANTS = {"unfused": UNFUSED, "A": FUSE_A, "B": FUSE_B, "C": FUSE_C, "direct": FUSE_DIRECT}
-PER_BLOCK, BATCHED = 0, 1
-LAUNCHES = {"per_block": PER_BLOCK, "batched": BATCHED}
+PER_BLOCK, BATCHED, PERSISTENT = 0, 1, 2
+LAUNCHES = {"per_block": PER_BLOCK, "batched": BATCHED, "persistent": PERSISTENT}
 XCHG_AUTO, XCHG_NCCL, XCHG_P2P, XCHG_HOST = 0, 1, 2, 3
 EXCHANGES = {"auto": XCHG_AUTO, "nccl": XCHG_NCCL, "p2p": XCHG_P2P, "host": XCHG_HOST}
 INIT_DEFAULT, INIT_CONST, INIT_LINEAR, INIT_HASH = 0, 1, 2, 3

@@ -80,3 +80,26 @@ def test_plan_peer_faces():
     for n, g, want in ((1, (1536,) * 3, 0), (2, (1536, 1536, 3072), 1), (4, (1536, 3072, 3072), 2),
                        (8, (3072,) * 3, 3)):
         assert j3d.plan(g, n_gpus=n)["peer_faces_max"] == want
+
+
+def test_persistent_launch_validation():
+    """J3D_PERSISTENT is the direct variant on one GPU without graphs; anything
+    else is rejected by the shared config check (jacobi3d_plan, no GPU)."""
+    import paper_2202_11819_b200 as j3d
+    from paper_2202_11819_b200 import jacobi3d as jb
+
+    def rc(**kw):
+        cfg = jb.make_config((16, 16, 16), **kw)
+        return jb.lib.jacobi3d_plan(ctypes.byref(cfg), ctypes.byref(jb.PlanInfo()))
+
+    assert jb.LAUNCHES["persistent"] == jb.PERSISTENT == 2
+    assert rc(variant="direct", launch="persistent") == 0
+    assert rc(variant="direct", launch="persistent", odf=8) == 0
+    assert rc(variant="unfused", launch="persistent") == jb.EINVAL
+    assert rc(variant="C", launch="persistent") == jb.EINVAL
+    assert rc(variant="direct", launch="persistent", graph=True) == jb.EINVAL
+    assert rc(variant="direct", launch="persistent", n_gpus=2) == jb.EINVAL
+    cfg = jb.make_config((16, 16, 16))
+    cfg.launch = 3
+    assert jb.lib.jacobi3d_plan(ctypes.byref(cfg), ctypes.byref(jb.PlanInfo())) == jb.EINVAL
+    del j3d
