@@ -29,7 +29,9 @@ METRIC = "Jacobi3D GLUPS and ms/iter at 1/2/4/8 B200; achieved HBM GB/s vs peak"
 SEED = 20220223
 BYTES_PER_LUP = 16.0  # algorithmic HBM bytes per lattice-site update (read u^n + write u^{n+1}, fp64)
 
-# name -> (per-GPU or global, dims, odf, variant, launch, graph)
+L2_BYTES = 126.5e6  # B200 L2 (both dies)
+
+# name -> weak (per-GPU dims) or strong (global dims), odf
 WORKLOADS = {
     # configs[1]: weak scaling, 1536^3 per GPU, ODF=1
     "weak1536_odf1": dict(kind="weak", per_gpu=(1536, 1536, 1536), odf=1),
@@ -197,7 +199,7 @@ def main():
     odf = a.odf or wl["odf"]
     cfg_json = {"workload": a.workload, "grid": list(grid), "odf": odf, "variant": a.variant, "launch": a.launch,
                 "graph": bool(a.graph), "exchange": a.exchange, "overlap": bool(a.overlap), "n_gpus": n,
-                "l2": "inputs larger than L2 (no flush needed)" if grid[0] * grid[1] * grid[2] * 16 / n > 2e9
+                "l2": "inputs larger than L2 (no flush needed)" if grid[0] * grid[1] * grid[2] * 16 / n > L2_BYTES
                 else "inputs smaller than L2",
                 "init": f"hash-random [0,1), seed {SEED}, Dirichlet 1.0"}
 

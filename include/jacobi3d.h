@@ -80,9 +80,14 @@ extern "C" {
                                it reads (own block and neighbour blocks) finished iteration k,
                                tracked by on-device completion counters -- no launch, no
                                host sync and no grid-wide tail between iterations (PAPER.md
-                               L739-749: launch/sync overhead at fine granularity).  Requires
-                               variant J3D_FUSE_DIRECT, n_gpus == 1, use_graph == 0, else
-                               J3D_EINVAL                                                      */
+                               L739-749: launch/sync overhead at fine granularity).  Across
+                               GPUs the counters live in the IPC-mapped arena and a slab next
+                               to a peer waits on the peer's counter over NVLink; the epilogue
+                               stores every peer face straight into the peer's ghost layer
+                               (no exchange kernels, no host-side epochs); the call ends with
+                               a wait until the peers' writes into this GPU have landed.
+                               Requires variant J3D_FUSE_DIRECT, use_graph == 0 and, for
+                               n_gpus > 1, exchange AUTO / P2P; else J3D_EINVAL              */
 
 /* ---- exchange backend between GPUs (same-GPU faces are always LOCAL) ---- */
 #define J3D_XCHG_AUTO    0  /* P2P when every peer is reachable over NVLink, else NCCL          */

@@ -37,8 +37,10 @@ int validate_cfg(const jacobi3d_config* c) {
     if (c->variant < J3D_UNFUSED || c->variant > J3D_FUSE_DIRECT) return fail(J3D_EINVAL, "unknown variant");
     if (c->launch != J3D_PER_BLOCK && c->launch != J3D_BATCHED && c->launch != J3D_PERSISTENT)
         return fail(J3D_EINVAL, "unknown launch mode");
-    if (c->launch == J3D_PERSISTENT && (c->variant != J3D_FUSE_DIRECT || c->n_gpus != 1 || c->use_graph != 0))
-        return fail(J3D_EINVAL, "J3D_PERSISTENT needs variant J3D_FUSE_DIRECT, n_gpus == 1 and use_graph == 0");
+    if (c->launch == J3D_PERSISTENT &&
+        (c->variant != J3D_FUSE_DIRECT || c->use_graph != 0 ||
+         (c->n_gpus > 1 && c->exchange != J3D_XCHG_AUTO && c->exchange != J3D_XCHG_P2P)))
+        return fail(J3D_EINVAL, "J3D_PERSISTENT needs variant J3D_FUSE_DIRECT, use_graph == 0 and P2P exchange");
     if (c->exchange < J3D_XCHG_AUTO || c->exchange > J3D_XCHG_HOST) return fail(J3D_EINVAL, "unknown exchange backend");
     if (c->n_gpus < 1 || c->rank < 0 || c->rank >= c->n_gpus) return fail(J3D_EINVAL, "rank / n_gpus out of range");
     if (c->odf < 1) return fail(J3D_EINVAL, "odf must be >= 1");
@@ -132,7 +134,7 @@ int jacobi3d_create(const jacobi3d_config* cfg, const uint8_t* nccl_uid, jacobi3
         c->overlap = cfg->overlap && cfg->launch == J3D_BATCHED && c->n_gpus > 1 &&
                      std::any_of(c->has_peer.begin(), c->has_peer.end(), [](uint8_t h) { return h != 0; });
         CK(cudaMalloc(&c->arena, (size_t)c->arena_bytes));
-        CK(cudaMemset(c->arena, 0, 4096));
+        CK(cudaMemset(c->arena, 0, (size_t)c->off_bufs));  // flags, scratch, persistent counters
         // face buffers start zeroed; done here, before any peer can map the
         // arena, so it can never race with a peer's NVLink stores
         CK(cudaMemset(c->arena + c->off_faces, 0, (size_t)(c->arena_bytes - c->off_faces)));
@@ -153,6 +155,9 @@ int jacobi3d_create(const jacobi3d_config* cfg, const uint8_t* nccl_uid, jacobi3
         if (const char* e = std::getenv("J3D_XSECTOR")) c->xsector_ok = std::atoi(e) != 0;
         if (const char* e = std::getenv("J3D_PEERX_DIRECT")) c->peer_x_direct = std::atoi(e) != 0;
         if (const char* e = std::getenv("J3D_PEERX_PACK")) c->peer_x_pack = std::atoi(e) != 0;
+        // a persistent launch has no separate kernels between iterations: every peer
+        // face, x included, is stored by the epilogue straight into the peer's ghost layer
+        if (cfg->launch == J3D_PERSISTENT) c->peer_x_direct = true;
         c->peer_base.assign(c->n_gpus, nullptr);
         build_static_tables(c);
         build_tables(c);

@@ -133,7 +133,7 @@ struct jacobi3d {
 
     // arena layout (identical on every rank)
     char* arena = nullptr;
-    int64_t arena_bytes = 0, off_flags = 0, off_scratch = 0, off_bufs = 0, buf_bytes = 0, off_faces = 0;
+    int64_t arena_bytes = 0, off_flags = 0, off_scratch = 0, off_done = 0, off_bufs = 0, buf_bytes = 0, off_faces = 0;
     std::array<int64_t, 6> face_bytes{};
     int64_t faces_per_block_bytes = 0;
     std::vector<char*> peer_base;  // mapped arenas (index = rank), nullptr for self
@@ -178,9 +178,12 @@ struct jacobi3d {
     int n_items = 0, tile_kind = 0, grid_cap = 0;
     // J3D_PERSISTENT: slab dependency tables and completion counters (device.cuh IterCtl)
     int32_t* d_item_slab = nullptr;             // [n_items]
-    int32_t* d_slab_deps = nullptr;             // [n_slabs][MAX_DEPS]
-    unsigned int* d_done = nullptr;             // [n_slabs]
-    int n_slabs = 0;
+    const unsigned int** d_slab_deps = nullptr;        // [n_slabs][MAX_DEPS] counter pointers (local / peer)
+    const unsigned int** d_slab_deps_local = nullptr;  // the same without the peer entries (skip_exchange)
+    const unsigned int** d_remote_done = nullptr;      // every peer counter some slab waits for
+    int n_remote_done = 0;
+    unsigned int* d_done = nullptr;             // [n_slabs], in the arena at off_done
+    int n_slabs = 0, persist_nzc = 0;
     uint32_t slab_target = 0;                   // consumer warps x tiles per slab
     uint32_t persist_base = 0;                  // iterations counted in d_done (mod 2^32)
     int persist_n = 0;                          // set while launching a persistent stencil
@@ -262,6 +265,7 @@ FaceRef recv_src(const jacobi3d* c, int l, int f, int par);
 FaceRef pack_dst(const jacobi3d* c, int l, int f, int par);
 void build_tables(jacobi3d* c);
 void build_static_tables(jacobi3d* c);
+void build_persist_deps(jacobi3d* c);
 
 // launch.cu
 cudaEvent_t pool_event(jacobi3d* c);

@@ -57,13 +57,16 @@ struct WorkItem {
 // whose iteration-k-1 reads its writes would clobber -- has
 // done >= (base + k) * target.
 constexpr int MAX_DEPS = 9;
+constexpr int32_t SLAB_PEER = 1 << 30;      // item_slab flag: the slab touches a peer GPU's face
+constexpr int32_t SLAB_MASK = SLAB_PEER - 1;
 struct IterCtl {
-    const int32_t* item_slab;  // [n_items]
-    const int32_t* slab_deps;  // [n_slabs][MAX_DEPS], -1 padded
-    unsigned int* done;        // [n_slabs]; nullptr: one iteration, no tracking
-    int32_t n_iter;            // iterations in this launch
-    uint32_t target;           // completions per slab per iteration (consumer warps x tiles per slab)
-    uint32_t base;             // iterations counted in done[] before this launch
+    const int32_t* item_slab;               // [n_items] slab index | SLAB_PEER
+    const unsigned int* const* slab_deps;   // [n_slabs][MAX_DEPS] counters, null padded; bit 0 set: a peer's
+    unsigned int* done;                     // [n_slabs]; nullptr: one iteration, no tracking
+    int32_t n_iter;                         // iterations in this launch
+    uint32_t target;                        // completions per slab per iteration (consumer warps x tiles per slab)
+    uint32_t base;                          // iterations counted in done[] before this launch
+    int32_t sys;                            // 1: some slabs wait on peer counters (iteration 0 waits too)
 };
 
 // A strided 2D face copy (pack: owned layer -> send buffer / peer receive

@@ -62,9 +62,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ uint32_t ld_acquire_u32(const unsigned int* p) {
+__device__ __forceinline__ uint32_t ld_acquire_u32(const unsigned int* p, bool sys) {
     uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    if (sys) asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    else asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 __device__ __forceinline__ uint64_t global_ns() {
@@ -77,18 +78,23 @@ __device__ __forceinline__ uint64_t global_ns() {
 // finished `iters` iterations (IterCtl, device.cuh), then order the async
 // proxy (TMA) after the acquired generic-proxy writes.  A wait beyond 60 s
 // can only be a bug: trap rather than hang the GPU.
+__device__ __forceinline__ void wait_counter(const unsigned int* p, uint32_t need, bool sys) {
+    if ((int32_t)(ld_acquire_u32(p, sys) - need) >= 0) return;
+    const uint64_t t0 = global_ns();
+    while ((int32_t)(ld_acquire_u32(p, sys) - need) < 0) {
+        __nanosleep(128);
+        if (global_ns() - t0 > 60ull * 1000000000ull) __trap();
+    }
+}
+
 __device__ __noinline__ void wait_slabs(const IterCtl ctl, int it, uint32_t iters) {
     const uint32_t need = iters * ctl.target;
-    const int32_t* dp = ctl.slab_deps + (int64_t)ctl.item_slab[it] * MAX_DEPS;
+    const unsigned int* const* dp = ctl.slab_deps + (int64_t)(ctl.item_slab[it] & SLAB_MASK) * MAX_DEPS;
     for (int j = 0; j < MAX_DEPS; ++j) {
-        const int t = dp[j];
-        if (t < 0) break;
-        if ((int32_t)(ld_acquire_u32(ctl.done + t) - need) >= 0) continue;
-        const uint64_t t0 = global_ns();
-        while ((int32_t)(ld_acquire_u32(ctl.done + t) - need) < 0) {
-            __nanosleep(128);
-            if (global_ns() - t0 > 60ull * 1000000000ull) __trap();
-        }
+        const uintptr_t p = reinterpret_cast<uintptr_t>(dp[j]);
+        if (!p) break;
+        // bit 0 tags a peer GPU's counter: acquire at system scope
+        wait_counter(reinterpret_cast<const unsigned int*>(p & ~uintptr_t(1)), need, (p & 1) != 0);
     }
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -373,7 +379,9 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                 if (g < 0) break;
                 const int k = g / n_items, it = g - k * n_items;
                 const WorkItem w = items[it];
-                if (k > 0) wait_slabs(ctl, it, ctl.base + (uint32_t)k);
+                // iteration 0 of a call waits only for peers (this GPU's previous
+                // launch is complete in stream order)
+                if (ctl.done && (k > 0 || ctl.sys)) wait_slabs(ctl, it, ctl.base + (uint32_t)k);
                 const CUtensorMap* tm = tmaps + (2 * w.blk + (parity ^ (k & 1)));
                 tmap_acquire(tm);
                 const int c0 = XOFF + w.tx * T::TX - T::HX, c1 = w.ty * T::TY;
@@ -764,11 +772,25 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
             mbar_arrive(&empty[sc]);  // plane z1
         }
         if (ctl.done) {  // persistent launch: publish this warp's part of the item (release)
-            __threadfence();
+            const int sv = ctl.item_slab[it];
+            // slabs next to a peer GPU (they stored into its ghost layer; it reads their
+            // counter over NVLink) release at system scope, the others at GPU scope
+            if (sv & SLAB_PEER) __threadfence_system();
+            else __threadfence();
             __syncwarp();
-            if (lane == 0) atomicAdd(ctl.done + ctl.item_slab[it], 1u);
+            if (lane == 0) atomicAdd(ctl.done + (sv & SLAB_MASK), 1u);
         }
     }
+}
+
+// ------------------------------------------------------------------ persistent: end of a call
+// Wait until every peer counter this GPU's slabs depend on reached `need`:
+// the peers' epilogue stores into this GPU's ghost layers for the call's
+// iterations have all landed when this kernel completes.
+__global__ void __launch_bounds__(32) wait_counters_kernel(const unsigned int* const* __restrict__ ptrs, int n,
+                                                          uint32_t need) {
+    for (int i = threadIdx.x; i < n; i += 32) wait_counter(ptrs[i], need, true);
+    __threadfence_system();
 }
 
 // ------------------------------------------------------------------ face copies
@@ -977,6 +999,12 @@ cudaError_t stencil_occupancy(int kind, bool, int* blocks_per_sm) {
 
 int stencil_box_w(int kind) { return tile_shape(kind).tx + 8; }
 int stencil_box_h(int kind) { return tile_shape(kind).ty + 2; }
+
+cudaError_t launch_wait_counters(const unsigned int* const* ptrs, int n, uint32_t need, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    wait_counters_kernel<<<1, 32, 0, st>>>(ptrs, n, need);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_copy_faces(const CopyDesc* d, int per_group, int groups, int64_t max_cells, cudaStream_t st) {
     if (groups <= 0 || max_cells <= 0) return cudaSuccess;

@@ -41,10 +41,12 @@ void stencil(jacobi3d* c, int begin, int count, int parity, cudaStream_t st, int
     L.kind = c->tile_kind;
     L.faces = c->faces_fused;
     L.sched = c->d_sched + 2 * (l + 1);  // one counter pair per concurrently running launch
-    L.ctl = IterCtl{nullptr, nullptr, nullptr, 1, 0, 0};
+    L.ctl = IterCtl{nullptr, nullptr, nullptr, 1, 0, 0, 0};
     const int n_iter = c->persist_n;
     if (n_iter > 0) {  // J3D_PERSISTENT: n_iter iterations in this one launch
-        L.ctl = IterCtl{c->d_item_slab, c->d_slab_deps, c->d_done, n_iter, c->slab_target, c->persist_base};
+        const bool remote = c->n_remote_done > 0 && !c->skip_exchange;
+        L.ctl = IterCtl{c->d_item_slab, remote ? c->d_slab_deps : c->d_slab_deps_local, c->d_done, n_iter,
+                        c->slab_target, c->persist_base, remote ? 1 : 0};
         L.grid = c->grid_cap;
     }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -273,6 +275,11 @@ void do_iterate(jacobi3d* c, int64_t n) {
             stencil(c, 0, c->n_items, (int)(c->iter & 1), c->main, -1);
             c->persist_n = 0;
             c->persist_base += (uint32_t)m;
+            if (c->n_remote_done > 0 && !c->skip_exchange) {  // peers' writes into this GPU have landed
+                CK(launch_wait_counters(c->d_remote_done, c->n_remote_done, c->persist_base * c->slab_target,
+                                        c->main));
+                count_launch(c, -1);
+            }
             c->iter += m;
             c->iter_since_set += m;
             c->stat_iters += m;
@@ -335,7 +342,8 @@ void destroy_ctx(jacobi3d* c) {
     cudaFree(c->d_push);
     cudaFree(c->d_item_slab);
     cudaFree(c->d_slab_deps);
-    cudaFree(c->d_done);
+    cudaFree(c->d_slab_deps_local);
+    cudaFree(c->d_remote_done);
     cudaFree(c->d_pack_peer);
     cudaFree(c->d_unpack_peer);
     cudaFree(c->d_pack_local);

@@ -21,7 +21,11 @@ void build_layout(jacobi3d* c) {
     for (int f = 0; f < 6; ++f) c->faces_per_block_bytes += 4 * c->face_bytes[f];  // send/recv x 2 parities
     c->off_flags = 0;
     c->off_scratch = 2048;
-    c->off_bufs = 4096;
+    // J3D_PERSISTENT slab completion counters (at most one slab per plane of each
+    // local block); inside the arena so peers read them over NVLink
+    c->off_done = 4096;
+    const int64_t done_bytes = c->cfg.launch == J3D_PERSISTENT ? (int64_t)c->n_local * c->nz * 4 : 0;
+    c->off_bufs = align_up(c->off_done + done_bytes, 4096);
     c->off_faces = c->off_bufs + (int64_t)c->n_local * 2 * c->buf_bytes;
     c->arena_bytes = c->off_faces + (int64_t)c->n_local * c->faces_per_block_bytes;
 }
@@ -229,6 +233,57 @@ void build_tables(jacobi3d* c) {
         CK(cudaMemcpy(c->d_pack_local, pk_loc.data(), pk_loc.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(c->d_unpack_local, up_loc.data(), up_loc.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
     }
+    build_persist_deps(c);
+}
+
+// J3D_PERSISTENT dependency tables (IterCtl, device.cuh).  The slabs an item
+// of slab (l, zc) waits for: its block's own and adjacent z chunks, the same
+// chunk of every x/y neighbour block, and for an edge chunk the z neighbour's
+// edge chunk it exchanges a ghost plane with.  A neighbour on a peer GPU is
+// named by a pointer into that rank's IPC-mapped arena (remote counters),
+// known only after jacobi3d_ipc_connect; `remote` collects those pointers for
+// the end-of-call wait.  The second table drops every remote entry (timing
+// with the exchange elided, jacobi3d_set_skip_exchange).
+void build_persist_deps(jacobi3d* c) {
+    if (c->cfg.launch != J3D_PERSISTENT) return;
+    const int nl = c->n_local, nzc = c->persist_nzc;
+    std::vector<const unsigned int*> deps((size_t)c->n_slabs * MAX_DEPS, nullptr), local(deps);
+    std::vector<const unsigned int*> remote;
+    auto counter = [&](int l, int f, int zc) -> const unsigned int* {
+        if (c->kind[l][f] == LOCAL) return c->d_done + c->nbr_local[l][f] * nzc + zc;
+        if (c->kind[l][f] != PEER_P2P || !c->p2p_connected) return nullptr;
+        const int r = c->plan.blocks[c->plan.blocks[c->gid[l]].nbr[f]].owner;
+        const uintptr_t p = (uintptr_t)((const unsigned int*)(c->peer_base[r] + c->off_done) + c->nbr_local[l][f] * nzc + zc);
+        return (const unsigned int*)(p | 1);  // tag: system-scope acquire (device.cuh)
+    };
+    for (int l = 0; l < nl; ++l)
+        for (int zc = 0; zc < nzc; ++zc) {
+            const unsigned int** d = &deps[(size_t)(l * nzc + zc) * MAX_DEPS];
+            const unsigned int** dl = &local[(size_t)(l * nzc + zc) * MAX_DEPS];
+            int n = 0, nloc = 0;
+            auto add = [&](const unsigned int* p, bool is_local) {
+                if (!p) return;
+                if (n == MAX_DEPS) throw Error(J3D_EUNSUPPORTED, "slab dependency table overflow");
+                d[n++] = p;
+                if (is_local) dl[nloc++] = p;
+                else if (std::find(remote.begin(), remote.end(), p) == remote.end()) remote.push_back(p);
+            };
+            for (int dz = -1; dz <= 1; ++dz)
+                if (zc + dz >= 0 && zc + dz < nzc) add(c->d_done + l * nzc + zc + dz, true);
+            for (int f = 0; f < 4; ++f) add(counter(l, f, zc), c->kind[l][f] == LOCAL);
+            if (zc == 0) add(counter(l, 4, nzc - 1), c->kind[l][4] == LOCAL);
+            if (zc == nzc - 1) add(counter(l, 5, 0), c->kind[l][5] == LOCAL);
+        }
+    for (auto& p : remote) p = (const unsigned int*)((uintptr_t)p & ~uintptr_t(1));
+    CK(cudaMemcpy(c->d_slab_deps, deps.data(), deps.size() * sizeof(void*), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_slab_deps_local, local.data(), local.size() * sizeof(void*), cudaMemcpyHostToDevice));
+    cudaFree(c->d_remote_done);
+    c->d_remote_done = nullptr;
+    c->n_remote_done = (int)remote.size();
+    if (!remote.empty()) {
+        CK(cudaMalloc(&c->d_remote_done, remote.size() * sizeof(void*)));
+        CK(cudaMemcpy(c->d_remote_done, remote.data(), remote.size() * sizeof(void*), cudaMemcpyHostToDevice));
+    }
 }
 
 void build_static_tables(jacobi3d* c) {
@@ -346,6 +401,22 @@ void build_static_tables(jacobi3d* c) {
     if (c->overlap) {  // BATCHED only: exterior items of every block first (stable order otherwise)
         std::stable_partition(items.begin(), items.end(), exterior);
         c->n_ext = (int)std::count_if(items.begin(), items.end(), exterior);
+    } else if (c->cfg.launch == J3D_PERSISTENT && c->n_gpus > 1) {
+        // persistent: slabs that wait on a peer LAST -- the peer's matching slabs
+        // were the last of its previous iteration too, so a GPU may run up to an
+        // iteration ahead of a slower neighbour instead of meeting it at every
+        // iteration start.  Whole slabs move (a slab completes only with all its
+        // tiles, so splitting one would delay every dependant of it).
+        std::vector<uint8_t> ext_slab((size_t)nl * best_zc, 0);
+        auto zc_of = [&](const WorkItem& w) {
+            int zc = 0;
+            while ((int)(c->nz * (zc + 1) / best_zc) <= w.z0) ++zc;
+            return zc;
+        };
+        for (const WorkItem& w : items)
+            if (exterior(w)) ext_slab[(size_t)w.blk * best_zc + zc_of(w)] = 1;
+        std::stable_partition(items.begin(), items.end(),
+                              [&](const WorkItem& w) { return !ext_slab[(size_t)w.blk * best_zc + zc_of(w)]; });
     }
     c->n_items = (int)items.size();
     c->item_cells.assign(items.size() + 1, 0);
@@ -356,37 +427,30 @@ void build_static_tables(jacobi3d* c) {
         c->item_cells[i + 1] = c->item_cells[i] + ex * ey * (w.z1 - w.z0);
     }
     if (c->cfg.launch == J3D_PERSISTENT) {
-        // slab = (local block, z chunk); deps of a slab (IterCtl, device.cuh): its own and the
-        // adjacent z chunks of the block, the same chunk of the x/y neighbour blocks, and for
-        // an edge chunk the z neighbour's edge chunk it exchanges a ghost plane with
+        // slab = (local block, z chunk); the dependency tables are built by build_persist_deps
         const int nzc = (int)best_zc;
+        if (nzc > c->nz) throw Error(J3D_EUNSUPPORTED, "more z chunks than planes");
+        c->persist_nzc = nzc;
         c->n_slabs = nl * nzc;
         c->slab_target = (uint32_t)(ts.ncw * ntx * nty);
-        std::vector<int32_t> slab(items.size()), deps((size_t)c->n_slabs * MAX_DEPS, -1);
+        std::vector<int32_t> slab(items.size());
         for (size_t i = 0; i < items.size(); ++i) {
             const WorkItem& w = items[i];
             int zc = 0;
             while ((int)(c->nz * (zc + 1) / best_zc) <= w.z0) ++zc;
-            slab[i] = w.blk * nzc + zc;
-        }
-        for (int l = 0; l < nl; ++l)
-            for (int zc = 0; zc < nzc; ++zc) {
-                int32_t* d = &deps[(size_t)(l * nzc + zc) * MAX_DEPS];
-                int n = 0;
-                for (int dz = -1; dz <= 1; ++dz)
-                    if (zc + dz >= 0 && zc + dz < nzc) d[n++] = l * nzc + zc + dz;
-                for (int f = 0; f < 4; ++f)
-                    if (c->kind[l][f] == LOCAL) d[n++] = c->nbr_local[l][f] * nzc + zc;
-                if (zc == 0 && c->kind[l][4] == LOCAL) d[n++] = c->nbr_local[l][4] * nzc + (nzc - 1);
-                if (zc == nzc - 1 && c->kind[l][5] == LOCAL) d[n++] = c->nbr_local[l][5] * nzc;
-                if (n > MAX_DEPS) throw Error(J3D_EUNSUPPORTED, "slab dependency table overflow");
+            // slab flag SLAB_PEER: some item of the slab touches a peer face
+            bool peer = false;
+            for (int f = 0; f < 6 && !peer; ++f) {
+                if (!is_peer(w.blk, f)) continue;
+                peer = f < 4 || (f == 4 && zc == 0) || (f == 5 && zc == nzc - 1);
             }
+            slab[i] = (w.blk * nzc + zc) | (peer ? SLAB_PEER : 0);
+        }
         CK(cudaMalloc(&c->d_item_slab, std::max<size_t>(1, slab.size()) * sizeof(int32_t)));
         CK(cudaMemcpy(c->d_item_slab, slab.data(), slab.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-        CK(cudaMalloc(&c->d_slab_deps, deps.size() * sizeof(int32_t)));
-        CK(cudaMemcpy(c->d_slab_deps, deps.data(), deps.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-        CK(cudaMalloc(&c->d_done, (size_t)c->n_slabs * sizeof(unsigned int)));
-        CK(cudaMemset(c->d_done, 0, (size_t)c->n_slabs * sizeof(unsigned int)));
+        CK(cudaMalloc(&c->d_slab_deps, (size_t)c->n_slabs * MAX_DEPS * sizeof(void*)));
+        CK(cudaMalloc(&c->d_slab_deps_local, (size_t)c->n_slabs * MAX_DEPS * sizeof(void*)));
+        c->d_done = (unsigned int*)(c->arena + c->off_done);  // zeroed with the arena at create
         c->persist_base = 0;
     }
     CK(cudaMalloc(&c->d_items, std::max<size_t>(1, items.size()) * sizeof(WorkItem)));

@@ -1,0 +1,14 @@
+mkdir -p gpurun_out
+N=$(nvidia-smi -L | wc -l)
+timeout 600 python -m pytest tests/test_gpu_persistent.py -x -q 2>&1 | tail -3
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29512 tests/mp_worker.py persistent 2>&1 | grep -E "MP OK|FAIL|Error|error" | head -20
+run() { timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus $N --warmup 5 --steps 60 --no-cpu --no-e2e "$@" > gpurun_out/b.log 2>&1; echo "bench $N $* rc=$? $(tail -1 gpurun_out/b.log | python -c "
+import json,sys
+d=json.loads(sys.stdin.read()); print(d['value'], round(d['value']/d['n_gpus'],1), d['ms_per_step'], d.get('halo'), (d.get('roofline') or {}).get('frac'), d['clocks']['sm_mhz'], d['gpu_launches'])" 2>&1)"; }
+run
+run --launch persistent
+run --workload fine384_odf64
+run --workload fine384_odf64 --launch persistent
+run --workload small192_odf1 --steps 500
+run --workload small192_odf1 --steps 500 --launch persistent
+run --grid 3072,1536,1536 --launch persistent

@@ -20,12 +20,14 @@ from oracle import core  # noqa: E402
 from paper_2202_11819_b200 import dist as jdist  # noqa: E402
 
 
-def run_case(grid, odf, variant, launch, graph, exchange, n, kind, seed, overlap=False):
+def run_case(grid, odf, variant, launch, graph, exchange, n, kind, seed, overlap=False, calls=None):
     ctx = jdist.create(grid, odf=odf, variant=variant, launch=launch, graph=graph, exchange=exchange,
                        overlap=overlap)
     try:
         ctx.init(kind, seed=seed)
-        ctx.iterate(n)
+        for m in (calls or [n]):
+            ctx.iterate(m)
+        n = sum(calls) if calls else n
         ctx.synchronize()
         got = ctx.gather_local()
         ck = ctx.checksum()
@@ -64,8 +66,9 @@ def run_fullsize(world):
     rank = dist.get_rank()
     rng = np.random.default_rng(100 + rank)
     checked = 0
-    for odf, variant, exchange in ((1, "direct", "p2p"), (8, "unfused", "nccl")):
-        ctx = jdist.create(grid, odf=odf, variant=variant, exchange=exchange)
+    for odf, variant, exchange, launch in ((1, "direct", "p2p", "batched"), (8, "unfused", "nccl", "batched"),
+                                           (1, "direct", "p2p", "persistent")):
+        ctx = jdist.create(grid, odf=odf, variant=variant, exchange=exchange, launch=launch)
         try:
             ctx.init("hash", seed=seed)
             ctx.iterate(n)
@@ -97,14 +100,14 @@ def run_fullsize(world):
     return checked
 
 
-def run_set_block_case(grid, odf, variant, exchange):
+def run_set_block_case(grid, odf, variant, exchange, launch="batched"):
     """Host upload on every rank (jacobi3d_set_block), collective refresh, run;
     iterate before the refresh must fail with J3D_ESTATE on multi-GPU."""
     from inputs.generators import uniform_field
     import paper_2202_11819_b200 as j3d
 
     U0 = uniform_field(*grid, seed=17, boundary=0.25)
-    ctx = jdist.create(grid, odf=odf, variant=variant, exchange=exchange, boundary=0.25)
+    ctx = jdist.create(grid, odf=odf, variant=variant, exchange=exchange, boundary=0.25, launch=launch)
     try:
         ctx.init("default")
         ctx.scatter_local(U0[1:-1, 1:-1, 1:-1])
@@ -202,6 +205,12 @@ def main():
                                                     [False, True]):
         cases.append((g, 4, variant, launch, graph, "host", 6, "hash", 4))
     cases.append((gx, 2, "direct", "batched", False, "host", 6, "hash", 4, True))
+    # persistent launches: in-kernel slab dependencies over NVLink, no host epochs
+    for grid_, odf_ in ((g, 4), (g, 1), (gx, 2), ((45, 34, 44), 2)):
+        for n_ in (1, 6, 13):
+            cases.append((grid_, odf_, "direct", "persistent", False, "p2p", n_, "hash", 7))
+    cases.append((g, 8, "direct", "persistent", False, "auto", 0, "hash", 8, False, [2, 0, 1, 5, 3]))
+    cases.append((g, 1, "direct", "persistent", False, "p2p", 30, "default", 0))
     cases.append(((45, 34, 44), 2, "direct", "batched", False, "p2p", 7, "hash", 1))
     cases.append(((45, 34, 44), 2, "C", "per_block", False, "nccl", 7, "hash", 1))
     if which == "fullsize":
@@ -212,21 +221,30 @@ def main():
         return
     if which == "xsplit":
         cases = [c for c in cases if c[0] == gx]
+    if which == "persistent":
+        cases = [c for c in cases if c[3] == "persistent"]
+        for zc in ("1", "3"):  # many thin slabs: long dependency chains across GPUs
+            os.environ["J3D_ZCHUNK"] = zc
+            try:
+                run_case(g, 4, "direct", "persistent", False, "p2p", 40, "hash", 9)
+            finally:
+                os.environ.pop("J3D_ZCHUNK", None)
     if which == "debug":
         cases = [((16, 8, 16), 1, "direct", "batched", False, "p2p", n_, "hash", 3) for n_ in (0, 1, 2, 3)]
         cases += [((16, 8, 16), 1, v, "batched", False, "p2p", 2, "hash", 3) for v in ("unfused", "C")]
         cases += [((16, 8, 16), 1, v, "batched", False, "host", 2, "hash", 3) for v in ("unfused", "direct")]
     n, failed = 0, []
-    if which not in ("debug", "xsplit"):
+    if which not in ("debug", "xsplit", "persistent"):
         try:
             run_api_case(g)
         except AssertionError as e:
             failed.append(str(e))
             print("FAIL", e, flush=True)
         n += 1
-        for v, x in (("direct", "p2p"), ("unfused", "nccl"), ("C", "host")):
+        for v, x, la in (("direct", "p2p", "batched"), ("unfused", "nccl", "batched"), ("C", "host", "batched"),
+                         ("direct", "p2p", "persistent")):
             try:
-                run_set_block_case(g, 2, v, x)
+                run_set_block_case(g, 2, v, x, la)
             except AssertionError as e:
                 failed.append(str(e))
                 print("FAIL", e, flush=True)
