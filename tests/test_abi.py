@@ -83,8 +83,9 @@ def test_plan_peer_faces():
 
 
 def test_persistent_launch_validation():
-    """J3D_PERSISTENT is the direct variant on one GPU without graphs; anything
-    else is rejected by the shared config check (jacobi3d_plan, no GPU)."""
+    """J3D_PERSISTENT is the direct variant without graphs, across GPUs over P2P
+    only; anything else is rejected by the shared config check (jacobi3d_plan,
+    no GPU)."""
     import paper_2202_11819_b200 as j3d
     from paper_2202_11819_b200 import jacobi3d as jb
 
@@ -98,7 +99,10 @@ def test_persistent_launch_validation():
     assert rc(variant="unfused", launch="persistent") == jb.EINVAL
     assert rc(variant="C", launch="persistent") == jb.EINVAL
     assert rc(variant="direct", launch="persistent", graph=True) == jb.EINVAL
-    assert rc(variant="direct", launch="persistent", n_gpus=2) == jb.EINVAL
+    assert rc(variant="direct", launch="persistent", n_gpus=2) == 0             # P2P (auto) across GPUs
+    assert rc(variant="direct", launch="persistent", n_gpus=2, exchange="p2p") == 0
+    assert rc(variant="direct", launch="persistent", n_gpus=2, exchange="nccl") == jb.EINVAL
+    assert rc(variant="direct", launch="persistent", n_gpus=2, exchange="host") == jb.EINVAL
     cfg = jb.make_config((16, 16, 16))
     cfg.launch = 3
     assert jb.lib.jacobi3d_plan(ctypes.byref(cfg), ctypes.byref(jb.PlanInfo())) == jb.EINVAL
