@@ -61,6 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         defs = [f"-DJ3D_XOFF={os.environ['J3D_XOFF']}"] if os.environ.get("J3D_XOFF") else []
+        defs += [f"-D{d}" for d in os.environ.get("J3D_DEFS", "").split()]  # experiment builds only
         cmd = [NVCC, *ARCH, *FLAGS, *defs, "-I", inc, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")

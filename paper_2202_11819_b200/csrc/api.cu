@@ -141,6 +141,7 @@ int jacobi3d_create(const jacobi3d_config* cfg, const uint8_t* nccl_uid, jacobi3
         CK(cudaMalloc(&c->d_descs, sizeof(StencilDesc) * 2 * c->n_local));
         CK(cudaMalloc(&c->d_tmaps, sizeof(CUtensorMap) * 2 * c->n_local));
         CK(cudaMalloc(&c->d_tmaps_split, sizeof(CUtensorMap) * 4 * c->n_local));
+        CK(cudaMalloc(&c->d_tmaps_x, sizeof(CUtensorMap) * 2 * c->n_local));
         CK(cudaMalloc(&c->d_pack, sizeof(CopyDesc) * 12 * c->n_local));
         CK(cudaMalloc(&c->d_unpack, sizeof(CopyDesc) * 12 * c->n_local));
         CK(cudaMalloc(&c->d_unpack_nccl, sizeof(CopyDesc) * 12 * c->n_local));
@@ -152,7 +153,6 @@ int jacobi3d_create(const jacobi3d_config* cfg, const uint8_t* nccl_uid, jacobi3
         CK(cudaMalloc(&c->d_geom, sizeof(BlockGeom) * c->n_local));
         CK(cudaMalloc(&c->d_sched, sizeof(unsigned int) * 2 * (c->n_local + 1)));
         CK(cudaMemset(c->d_sched, 0, sizeof(unsigned int) * 2 * (c->n_local + 1)));
-        if (const char* e = std::getenv("J3D_XSECTOR")) c->xsector_ok = std::atoi(e) != 0;
         if (const char* e = std::getenv("J3D_PEERX_DIRECT")) c->peer_x_direct = std::atoi(e) != 0;
         if (const char* e = std::getenv("J3D_PEERX_PACK")) c->peer_x_pack = std::atoi(e) != 0;
         // a persistent launch has no separate kernels between iterations: every peer

@@ -125,6 +125,9 @@ struct jacobi3d {
     Plan plan;
     int rank = 0, n_gpus = 1, device = 0, sms = 148;
     int64_t nx = 0, ny = 0, nz = 0, pitch = 0, zs = 0, buf_elems = 0;
+    int64_t grid_bytes = 0;  // the ghosted 3D array of one buffer (256-B aligned)
+    int64_t xg_pitch = 0;    // x ghost arrays: doubles per z plane (ny rounded up to even)
+    int64_t xg_bytes = 0;    // one x ghost array (nz+2 planes), 256-B aligned
     int n_local = 0;
     std::vector<int64_t> gid;                 // local index -> global block id
     std::vector<std::array<int, 6>> kind;     // FaceKind per local block face
@@ -151,6 +154,7 @@ struct jacobi3d {
     StencilDesc* d_descs = nullptr;
     CUtensorMap* d_tmaps = nullptr;
     CUtensorMap* d_tmaps_split = nullptr;
+    CUtensorMap* d_tmaps_x = nullptr;  // [2*l + p] x ghost vectors of each buffer
     int tma_mode = 0;
     WorkItem* d_items = nullptr;
     CopyDesc* d_pack = nullptr;
@@ -169,7 +173,6 @@ struct jacobi3d {
     CopyDesc* d_push = nullptr;
     BlockGeom* d_geom = nullptr;
     unsigned int* d_sched = nullptr;            // [2*(n_local+1)] stencil work counters
-    bool xsector_ok = true;
     bool peer_x_pack = true;     // peer x faces packed from the output by the push kernel (J3D_PEERX_PACK=0:
                                  // captured by the stencil epilogue into the send buffer; tuning)
     bool peer_x_direct = false;  // J3D_PEERX_DIRECT=1: peer x ghosts stored over NVLink from the epilogue (tuning)  // J3D_XSECTOR=0 disables whole-sector x-ghost stores (tuning)
@@ -241,12 +244,16 @@ struct jacobi3d {
     }
     int64_t face_na(int f) const { return f < 2 ? ny : nx; }
     int64_t face_nb(int f) const { return f < 4 ? nz : ny; }
+    // x ghost array `side` (0: -x, 1: +x) of a block buffer; element (y, z) at
+    // [(z+1)*xg_pitch + y], z in [-1, nz] (device.cuh layout)
+    double* xghost(double* b, int side) const { return (double*)((char*)b + grid_bytes + side * xg_bytes); }
     // owned (ghost=false) or ghost layer of a block buffer on face f as a FaceRef over (a,b)
     FaceRef layer(double* b, int f, bool ghost) const {
         const int a = f >> 1;
         const int64_t n = a == 0 ? nx : a == 1 ? ny : nz;
         const int64_t c = (f & 1) ? (ghost ? n : n - 1) : (ghost ? -1 : 0);
         double* o = b + zs + pitch + XOFF;  // owned (0,0,0)
+        if (a == 0 && ghost) return FaceRef{xghost(b, f & 1) + xg_pitch, 1, xg_pitch};
         if (a == 0) return FaceRef{o + c, pitch, zs};
         if (a == 1) return FaceRef{o + c * pitch, 1, zs};
         return FaceRef{o + c * zs, 1, pitch};

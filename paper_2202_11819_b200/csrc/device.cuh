@@ -5,10 +5,19 @@
 //   a ghosted 3D array of (nz+2) planes x (ny+2) rows x pitch doubles.  Owned
 //   cell (x,y,z), x in [0,nx), lives at
 //       base[(z+1)*zs + (y+1)*pitch + XOFF + x],   zs = pitch*(ny+2)
-//   with the -x ghost at column XOFF-1 and the +x ghost at XOFF+nx.  XOFF = 16
-//   doubles puts every owned row on a 128-byte boundary (pitch is a multiple
-//   of 16 doubles and buffers are 256-byte aligned), so warps read and write
-//   whole 128-byte lines and 16-byte vector accesses are aligned.
+//   XOFF = 16 doubles puts every owned row on a 128-byte boundary (pitch is a
+//   multiple of 16 doubles and buffers are 256-byte aligned), so warps read
+//   and write whole 128-byte lines and 16-byte vector accesses are aligned.
+//   The y and z ghost layers are rows / planes of this array (y = -1, ny;
+//   z = -1, nz).  The x ghost layers are NOT columns of it: each buffer is
+//   followed by two x ghost arrays (-x, +x), element (y, z) at
+//       xg[side][(z+1)*xg_pitch + y],   xg_pitch = ny rounded up to even,
+//   so a ghost column costs no partially used 128-byte line per row (on
+//   96-wide blocks those lines were a third of the DRAM reads) and the
+//   neighbour's epilogue stores it contiguously in y.  The stencil's TMA
+//   map starts at the owned column 0 and ends at nx - 1 (the halo columns
+//   beyond a block edge are zero-filled out of bounds) and a second map
+//   loads the x ghost vectors of the tile's rows.
 #pragma once
 #include <cstdint>
 
@@ -33,9 +42,7 @@ struct StencilDesc {
     uint32_t epi_mask;  // faces whose new boundary layer the epilogue stores to epi[f]
     int64_t pitch, zs;
     uint32_t pro_mask;  // faces whose ghost values the prologue reads from pro[f]
-    uint32_t xsector;   // bit f (f = 0, 1): epi[f] is an x ghost column of a buffer (layout above);
-                        // the epilogue may then write its whole 32-byte sector (ghost + 3 padding
-                        // columns) so no partial-sector read-modify-write reaches HBM
+    uint32_t pad0;
     FaceRef epi[6];
     FaceRef pro[6];
 };
@@ -83,6 +90,7 @@ struct BlockGeom {
     int64_t ox, oy, oz;  // global origin of owned cell (0,0,0)
     int32_t nx, ny, nz, pad;
     int64_t pitch, zs;
+    int64_t xg_off, xg_side, xg_pitch;  // x ghost arrays: buf + xg_off + side*xg_side (doubles)
 };
 
 }  // namespace j3d

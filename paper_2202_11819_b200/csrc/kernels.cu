@@ -136,21 +136,6 @@ __device__ __forceinline__ void st_global_v2(double* p, double a, double b) {
     asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
 }
 
-// Store one x-ghost value as its whole 32-byte sector.  q points at the ghost
-// cell; `left`: the ghost is the -x ghost (column XOFF-1, the last double of
-// its sector: columns XOFF-4..XOFF-2 are padding) else the +x ghost (column
-// XOFF+nx, first of its sector, nx % 4 == 0: the rest is row padding).
-__device__ __forceinline__ void st_ghost_sector(double* q, double v, bool left) {
-    double* b = left ? q - 3 : q;
-    if (left) {
-        st_global_v2(b, 0.0, 0.0);
-        st_global_v2(b + 2, 0.0, v);
-    } else {
-        st_global_v2(b, v, 0.0);
-        st_global_v2(b + 2, 0.0, 0.0);
-    }
-}
-
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     uint64_t z = x + 0x9E3779B97F4A7C15ULL;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -221,7 +206,11 @@ struct Tile {
                                            // 16-B aligned interior, rows a multiple of 64 B
     static constexpr int H = TY + 2;  // y0-1 .. y0+TY
     static constexpr uint32_t TX_BYTES = W * H * 8;
-    static constexpr int STAGE_BYTES = (W * H * 8 + 127) / 128 * 128;
+    // x ghost vectors of the tile's rows after the box: -x at SIDE_OFF, +x at
+    // SIDE_OFF + SIDE_STRIDE (TMA destinations are 128-byte aligned)
+    static constexpr int SIDE_OFF = (W * H * 8 + 127) / 128 * 128;
+    static constexpr int SIDE_STRIDE = (TY * 8 + 127) / 128 * 128;
+    static constexpr int STAGE_BYTES = SIDE_OFF + 2 * SIDE_STRIDE;
     static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8 + 2 * 4 * 8 + 4 * 4 + 128;
     static constexpr int THREADS = 32 * (NCW + 1);
     // the consumers hold the stages of planes z-1, z, z+1; at least one more is in flight
@@ -332,8 +321,9 @@ __device__ __forceinline__ void epi_store(const StencilDesc* __restrict__ d, uin
 template <class T>
 __global__ void __launch_bounds__(T::THREADS, T::MINB)
     stencil_tma_kernel(const StencilDesc* __restrict__ descs, const CUtensorMap* __restrict__ tmaps,
-                       const CUtensorMap* __restrict__ tmaps3, const WorkItem* __restrict__ items, int n_items,
-                       int parity, int flags, unsigned int* __restrict__ sched, const IterCtl ctl) {
+                       const CUtensorMap* __restrict__ tmaps3, const CUtensorMap* __restrict__ tmapsx,
+                       const WorkItem* __restrict__ items, int n_items, int parity, int flags,
+                       unsigned int* __restrict__ sched, const IterCtl ctl) {
     constexpr int NCW = T::NCW, RPW = T::RPW, CPL = T::CPL, W = T::W, NSTAGE = T::NSTAGE, IQ = 4;
     // The kernel has no static shared memory, so the dynamic window starts at
     // shared offset 0 (1024-B aligned); indexing the __shared__ array directly
@@ -382,13 +372,22 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                 // iteration 0 of a call waits only for peers (this GPU's previous
                 // launch is complete in stream order)
                 if (ctl.done && (k > 0 || ctl.sys)) wait_slabs(ctl, it, ctl.base + (uint32_t)k);
-                const CUtensorMap* tm = tmaps + (2 * w.blk + (parity ^ (k & 1)));
+                const int bp = 2 * w.blk + (parity ^ (k & 1));
+                const CUtensorMap* tm = tmaps + bp;
+                const CUtensorMap* tx = tmapsx + bp;
                 tmap_acquire(tm);
-                const int c0 = XOFF + w.tx * T::TX - T::HX, c1 = w.ty * T::TY;
+                tmap_acquire(tx);
+                const int nxb = descs[bp].nx;
+                // tiles at a block x edge also load the x ghost vectors of their rows
+                const uint32_t xe = (w.tx == 0 ? 1u : 0u) | ((w.tx + 1) * T::TX >= nxb ? 2u : 0u);
+                const uint32_t bytes = T::TX_BYTES + (uint32_t)__popc(xe) * (T::TY * 8);
+                const int c0 = w.tx * T::TX - T::HX, c1 = w.ty * T::TY;
                 for (int z = w.z0 - 1; z <= w.z1; ++z) {
                     mbar_wait(&empty[s], ph ^ 1);
-                    mbar_expect_tx(&full[s], T::TX_BYTES);
+                    mbar_expect_tx(&full[s], bytes);
                     unsigned char* dst = smem + s * T::STAGE_BYTES;
+                    if (xe & 1u) tma_load_3d(dst + T::SIDE_OFF, tx, &full[s], c1, z + 1, 0);
+                    if (xe & 2u) tma_load_3d(dst + T::SIDE_OFF + T::SIDE_STRIDE, tx, &full[s], c1, z + 1, 1);
                     if (tma_mode == 0) {
                         tma_load_3d(dst, tm, &full[s], c0, c1, z + 1);
                     } else if (tma_mode == 1 || tma_mode == 2) {
@@ -457,6 +456,21 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
         // wait for the stage of plane zz, patch its ghosts (fused prologue) if needed
         auto acquire = [&](int zz) {
             mbar_wait(&full[s], ph);
+            if (touch & 3u) {
+                // block x edge: the ghost values of this warp's rows go from the
+                // stage's x ghost vectors into the row's halo column
+                if (lane < RPW) {
+                    double* st = stage(s);
+                    const double* side = reinterpret_cast<const double*>(smem + s * T::STAGE_BYTES + T::SIDE_OFF);
+                    const int r = warp * RPW + lane;
+                    if (touch & 1u) st[(r + 1) * W + T::HX - 1] = side[r];
+                    if (touch & 2u) st[(r + 1) * W + T::HX + (nx - x0)] = side[T::SIDE_STRIDE / 8 + r];
+#ifndef J3D_NO_XFENCE
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
+                }
+                __syncwarp();
+            }
             if ((pro & touch) || (zz < 0 && (pro & 16u)) || (zz >= nz && (pro & 32u))) {
                 patch_stage<T>(d, stage(s), zz, x0, y0, warp, lane);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -549,15 +563,13 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                     if constexpr (FACES) {
                         if (xmd && x == 0 && v0) {
                             // my -x face feeds the neighbour's +x ghost
-                            if (d->xsector & 1u) st_ghost_sector(xmd + y * xmsa, vx, false);
-                            else xmd[y * xmsa] = vx;
+                            xmd[y * xmsa] = vx;
                         }
                         if (xpd && v0) {
                             const bool hit0 = x == nx - 1, hit1 = x + 1 == nx - 1;
                             if (hit0 || hit1) {
                                 const double v = hit0 ? vx : vy;
-                                if (d->xsector & 2u) st_ghost_sector(xpd + y * xpsa, v, true);
-                                else xpd[y * xpsa] = v;
+                                xpd[y * xpsa] = v;
                             }
                         }
                         if (fm & ~3u) {
@@ -586,8 +598,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
 #pragma unroll
                     for (int r = 0; r < RPW; ++r)
                         if (yl + r < ny) {
-                            if (d->xsector & 1u) st_ghost_sector(q + (int64_t)(yl + r) * F.sa, cap0[r], false);
-                            else q[(int64_t)(yl + r) * F.sa] = cap0[r];
+                            q[(int64_t)(yl + r) * F.sa] = cap0[r];
                         }
                 }
                 if ((fm & 2u) && clast < CPL && lane == lane_last) {
@@ -596,8 +607,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
 #pragma unroll
                     for (int r = 0; r < RPW; ++r)
                         if (yl + r < ny) {
-                            if (d->xsector & 2u) st_ghost_sector(q + (int64_t)(yl + r) * F.sa, cap1[r], true);
-                            else q[(int64_t)(yl + r) * F.sa] = cap1[r];
+                            q[(int64_t)(yl + r) * F.sa] = cap1[r];
                         }
                 }
             }
@@ -698,8 +708,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
 #pragma unroll
                     for (int r = 0; r < RPW; ++r)
                         if (yl + r < ny) {
-                            if (d->xsector & 1u) st_ghost_sector(q + (int64_t)(yl + r) * F.sa, cap0[r], false);
-                            else q[(int64_t)(yl + r) * F.sa] = cap0[r];
+                            q[(int64_t)(yl + r) * F.sa] = cap0[r];
                         }
                 }
                 if ((fm & 2u) && klast < KPL && lane == lane_last) {
@@ -708,8 +717,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
 #pragma unroll
                     for (int r = 0; r < RPW; ++r)
                         if (yl + r < ny) {
-                            if (d->xsector & 2u) st_ghost_sector(q + (int64_t)(yl + r) * F.sa, cap1[r], true);
-                            else q[(int64_t)(yl + r) * F.sa] = cap1[r];
+                            q[(int64_t)(yl + r) * F.sa] = cap1[r];
                         }
                 }
             }
@@ -838,6 +846,14 @@ __global__ void __launch_bounds__(256) init_kernel(const BlockGeom* __restrict__
         } else {
             v = ghost ? boundary : 0.0;
         }
+        if (x < 0 || x == b.nx) {  // x ghost arrays (layout: device.cuh)
+            if (y >= 0 && y < b.ny) {
+                const int64_t o = b.xg_off + (x < 0 ? 0 : b.xg_side) + (int64_t)(z + 1) * b.xg_pitch + y;
+                b.buf[0][o] = v;
+                b.buf[1][o] = v;
+            }
+            continue;
+        }
         const int64_t o = (int64_t)(z + 1) * b.zs + (int64_t)(y + 1) * b.pitch + XOFF + x;
         b.buf[0][o] = v;
         b.buf[1][o] = v;
@@ -950,7 +966,7 @@ static cudaError_t launch_t(const StencilLaunch& L, cudaStream_t st) {
     }
     if (L.n_items <= 0) return cudaSuccess;
     stencil_tma_kernel<T><<<L.grid, T::THREADS, T::SMEM_BYTES, st>>>(
-        L.descs, L.tmaps, L.tmaps_split, L.items, L.n_items, L.parity,
+        L.descs, L.tmaps, L.tmaps_split, L.tmaps_x, L.items, L.n_items, L.parity,
         (L.faces ? 1 : 0) | ((L.tma_mode & 3) << 2), L.sched, L.ctl);
     return cudaGetLastError();
 }

@@ -18,6 +18,7 @@ struct StencilLaunch {
     const StencilDesc* descs;  // device, [2*n_local_blocks]
     const CUtensorMap* tmaps;  // device, [2*n_local_blocks], 64-B aligned
     const CUtensorMap* tmaps_split;  // device, [2*n_local_blocks][2]: box heights 2 and H-4 (tma_mode 3)
+    const CUtensorMap* tmaps_x;      // device, [2*n_local_blocks]: x ghost vectors (y, z, side), box TY x 1 x 1
     int tma_mode;            // 0 plain, 1 evict_first, 2 evict_last, 3 split rows (shared rows evict_last)
     const WorkItem* items;     // device
     int n_items;

@@ -33,6 +33,7 @@ void stencil(jacobi3d* c, int begin, int count, int parity, cudaStream_t st, int
     L.descs = c->d_descs;
     L.tmaps = c->d_tmaps;
     L.tmaps_split = c->d_tmaps_split;
+    L.tmaps_x = c->d_tmaps_x;
     L.tma_mode = c->tma_mode;
     L.items = c->d_items + begin;
     L.n_items = count;
@@ -335,6 +336,7 @@ void destroy_ctx(jacobi3d* c) {
     cudaFree(c->d_descs);
     cudaFree(c->d_tmaps);
     cudaFree(c->d_tmaps_split);
+    cudaFree(c->d_tmaps_x);
     cudaFree(c->d_items);
     cudaFree(c->d_pack);
     cudaFree(c->d_unpack);

@@ -15,7 +15,10 @@ void build_layout(jacobi3d* c) {
     c->pitch = align_up(XOFF + c->nx + 1, PITCH_ALIGN);
     c->zs = c->pitch * (c->ny + 2);
     c->buf_elems = c->zs * (c->nz + 2);
-    c->buf_bytes = align_up(c->buf_elems * 8, 256);
+    c->grid_bytes = align_up(c->buf_elems * 8, 256);
+    c->xg_pitch = align_up(c->ny, 2);  // TMA: row strides are multiples of 16 bytes
+    c->xg_bytes = align_up(c->xg_pitch * (c->nz + 2) * 8, 256);
+    c->buf_bytes = c->grid_bytes + 2 * c->xg_bytes;
     for (int f = 0; f < 6; ++f) c->face_bytes[f] = align_up(face_cells(P.ext, f) * 8, 256);
     c->faces_per_block_bytes = 0;
     for (int f = 0; f < 6; ++f) c->faces_per_block_bytes += 4 * c->face_bytes[f];  // send/recv x 2 parities
@@ -126,7 +129,6 @@ void build_tables(jacobi3d* c) {
                         if (k == PEER_P2P && !c->p2p_connected) continue;  // filled after ipc_connect
                         d.epi[f] = c->layer(c->buf(c->nbr_local[l][f], q, r), f ^ 1, true);
                         d.epi_mask |= 1u << f;
-                        if (f < 2 && (c->nx % 4) == 0 && XOFF % 4 == 0 && c->xsector_ok) d.xsector |= 1u << f;  // whole-sector x-ghost stores
                     } else if (v == J3D_FUSE_DIRECT && f < 2 && c->peer_x_pack) {
                         continue;  // peer x face: packed from the output by the push kernel
                     } else if (v == J3D_FUSE_DIRECT) {
@@ -291,10 +293,10 @@ void build_static_tables(jacobi3d* c) {
     // ---- tensor maps [2*l + p] over each input buffer
     g_drv.load();
     // 192x22 tiles (11 consumer warps, 5-stage ring, 1 CTA/SM) when they divide
-    // the block width, else 128x30 (15 consumer warps) for wide blocks, 96x8
+    // the block width, else 128x30 (15 consumer warps) for wide blocks, 96x16
     // one-cell-per-lane tiles for 96-wide blocks (BASELINE configs[4]) and
     // 64x16 (2 CTAs/SM, 6 stages) for other narrow ones.  Sweeps: profiles/.
-    c->tile_kind = (c->nx % 192 == 0) ? 0 : c->nx >= 128 ? 1 : (c->nx == 96) ? 14 : 4;
+    c->tile_kind = (c->nx % 192 == 0) ? 0 : c->nx >= 128 ? 1 : (c->nx == 96) ? 12 : 4;
     if (c->tile_kind <= 1) {  // small grids: the wide tiles cannot keep every SM busy -> 64x16, 2 CTAs/SM
         const TileShape t = tile_shape(c->tile_kind);
         const int64_t tiles = ((c->nx + t.tx - 1) / t.tx) * ((c->ny + t.ty - 1) / t.ty) * nl;
@@ -313,28 +315,44 @@ void build_static_tables(jacobi3d* c) {
         promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
               : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     }
+    // over the owned columns only (x in [0, nx): the halo columns beyond a block
+    // edge are zero-filled out of bounds, never fetched) and every row / plane
+    // including the y / z ghost layers
     for (int l = 0; l < nl; ++l)
         for (int p = 0; p < 2; ++p) {
-            cuuint64_t dims[3] = {(cuuint64_t)(XOFF + c->nx + 1), (cuuint64_t)(c->ny + 2), (cuuint64_t)(c->nz + 2)};  // up to the +x ghost: the row padding is never fetched (TMA zero-fills beyond)
+            cuuint64_t dims[3] = {(cuuint64_t)c->nx, (cuuint64_t)(c->ny + 2), (cuuint64_t)(c->nz + 2)};
             cuuint64_t strides[2] = {(cuuint64_t)(c->pitch * 8), (cuuint64_t)(c->zs * 8)};
             cuuint32_t box[3] = {(cuuint32_t)stencil_box_w(c->tile_kind), (cuuint32_t)stencil_box_h(c->tile_kind), 1};
             cuuint32_t es[3] = {1, 1, 1};
-            DK(g_drv.encode(&maps[2 * l + p], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->buf(l, p), dims, strides, box, es,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+            DK(g_drv.encode(&maps[2 * l + p], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->buf(l, p) + XOFF, dims, strides,
+                            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
         }
     CK(cudaMemcpy(c->d_tmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+    // x ghost vectors: (y, z, side) over the two x ghost arrays of a buffer, box TY x 1 x 1
+    std::vector<CUtensorMap> xmaps(2 * nl);
+    for (int l = 0; l < nl; ++l)
+        for (int p = 0; p < 2; ++p) {
+            cuuint64_t dims[3] = {(cuuint64_t)c->ny, (cuuint64_t)(c->nz + 2), 2};
+            cuuint64_t strides[2] = {(cuuint64_t)(c->xg_pitch * 8), (cuuint64_t)c->xg_bytes};
+            cuuint32_t box[3] = {(cuuint32_t)ts.ty, 1, 1};
+            cuuint32_t es[3] = {1, 1, 1};
+            DK(g_drv.encode(&xmaps[2 * l + p], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->xghost(c->buf(l, p), 0), dims,
+                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+        }
+    CK(cudaMemcpy(c->d_tmaps_x, xmaps.data(), xmaps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
     // split maps: box heights 2 and H-4 (for the L2-policy split loads)
     std::vector<CUtensorMap> maps2(4 * nl);
     for (int l = 0; l < nl; ++l)
         for (int p = 0; p < 2; ++p)
             for (int h = 0; h < 2; ++h) {
-                cuuint64_t dims[3] = {(cuuint64_t)(XOFF + c->nx + 1), (cuuint64_t)(c->ny + 2), (cuuint64_t)(c->nz + 2)};  // up to the +x ghost: the row padding is never fetched (TMA zero-fills beyond)
+                cuuint64_t dims[3] = {(cuuint64_t)c->nx, (cuuint64_t)(c->ny + 2), (cuuint64_t)(c->nz + 2)};
                 cuuint64_t strides[2] = {(cuuint64_t)(c->pitch * 8), (cuuint64_t)(c->zs * 8)};
                 const int H = stencil_box_h(c->tile_kind);
                 cuuint32_t box[3] = {(cuuint32_t)stencil_box_w(c->tile_kind), (cuuint32_t)(h == 0 ? 2 : std::max(1, H - 4)), 1};
                 cuuint32_t es[3] = {1, 1, 1};
-                DK(g_drv.encode(&maps2[(2 * l + p) * 2 + h], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->buf(l, p), dims,
+                DK(g_drv.encode(&maps2[(2 * l + p) * 2 + h], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->buf(l, p) + XOFF, dims,
                                 strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
             }
@@ -470,6 +488,9 @@ void build_static_tables(jacobi3d* c) {
         geo[l].nz = (int32_t)c->nz;
         geo[l].pitch = c->pitch;
         geo[l].zs = c->zs;
+        geo[l].xg_off = c->grid_bytes / 8;
+        geo[l].xg_side = c->xg_bytes / 8;
+        geo[l].xg_pitch = c->xg_pitch;
     }
     CK(cudaMemcpy(c->d_geom, geo.data(), geo.size() * sizeof(BlockGeom), cudaMemcpyHostToDevice));
 }

@@ -216,3 +216,14 @@ def test_medium_grid_checksums_and_determinism():
                 ctx.iterate(30)
                 sums.append(ctx.checksum())
             assert sums == [want] * 3, (v, l, g)
+
+
+@pytest.mark.parametrize("kind", list(range(19)))
+def test_every_tile_kind(kind, monkeypatch):
+    """Every row of the kernel's tile table (J3D_TILE, kernels.cu J3D_TILES:
+    both lane maps, 1-3 CTAs/SM, 4-8 stages) on ragged multi-block grids, direct
+    and C variants (x ghost vectors, fused prologue/epilogue)."""
+    monkeypatch.setenv("J3D_TILE", str(kind))
+    _case((200, 45, 30), 2, "direct", "batched", False, 6, kind="hash", seed=kind + 1)
+    _case((96, 40, 24), 8, "C", "batched", False, 5, kind="hash", seed=kind + 2)
+    _case((45, 34, 22), 2, "unfused", "batched", False, 5, kind="hash", seed=kind + 3)
