@@ -42,6 +42,8 @@ WORKLOADS = {
     "weak1536_odf32": dict(kind="weak", per_gpu=(1536, 1536, 1536), odf=32),
     # configs[3]: strong scaling 3072^3 (needs >= 4 GPUs: 464 GB double-buffered)
     "strong3072_odf2": dict(kind="strong", global_=(3072, 3072, 3072), odf=2),
+    # SURVEY 8(d) config 4': strong scaling that reaches 1 GPU, 1536^3 global, ODF 8
+    "strong1536_odf8": dict(kind="strong", global_=(1536, 1536, 1536), odf=8),
     # configs[4]: fine-grained, 768^3 global (8 GPUs x ODF 64 = 96^3 blocks)
     "fine768_odf64": dict(kind="strong", global_=(768, 768, 768), odf=64),
     # configs[4] per GPU: 384^3 per GPU with ODF 64 = the 96^3 blocks of 768^3 on 8 GPUs
