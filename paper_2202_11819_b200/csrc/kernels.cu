@@ -953,7 +953,10 @@ cudaError_t launch_div7_selftest(uint64_t n, uint64_t seed, unsigned long long* 
     X(15, -96, 8, 1, 6, 3)  /* 96x8, 3 CTAs/SM                           */ \
     X(16, -96, 12, 1, 8, 2) /* 96x12                                     */ \
     X(17, -192, 11, 2, 5, 1) /* 192x22 one cell per lane                 */ \
-    X(18, -96, 6, 2, 8, 2)  /* 96x12 (RPW 2)                             */
+    X(18, -96, 6, 2, 8, 2)  /* 96x12 (RPW 2)                             */ \
+    X(19, 192, 12, 2, 4, 1) /* 192x24, 4 x 42 KB stages                  */ \
+    X(20, 192, 8, 2, 5, 1)  /* 192x16, 5 x 29 KB stages                  */ \
+    X(21, 192, 12, 2, 5, 1) /* 192x24, 5 stages                          */
 
 template <class T>
 static cudaError_t launch_t(const StencilLaunch& L, cudaStream_t st) {
@@ -981,7 +984,7 @@ static cudaError_t occ_t(int* blocks) {
 
 #define J3D_TYPE(k, tx, ncw, rpw, ns, mb) Tile<(tx > 0 ? tx : -tx), ncw, rpw, ns, mb, (tx > 0 ? 0 : 1)>
 
-int num_tile_kinds() { return 19; }
+int num_tile_kinds() { return 22; }
 
 TileShape tile_shape(int kind) {
     switch (kind) {

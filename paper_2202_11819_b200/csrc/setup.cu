@@ -297,6 +297,12 @@ void build_static_tables(jacobi3d* c) {
     // one-cell-per-lane tiles for 96-wide blocks (BASELINE configs[4]) and
     // 64x16 (2 CTAs/SM, 6 stages) for other narrow ones.  Sweeps: profiles/.
     c->tile_kind = (c->nx % 192 == 0) ? 0 : c->nx >= 128 ? 1 : (c->nx == 96) ? 12 : 4;
+    if (c->tile_kind == 0) {
+        // 192x24 (12 consumer warps) when 22-row tiles would leave a mostly empty last
+        // tile row: measured on 192x96x96 blocks 1144 -> 1248 GLUPS (4 GPUs), equal at 1536
+        auto waste = [&](int ty) { return (double)(((c->ny + ty - 1) / ty) * ty - c->ny) / (double)c->ny; };
+        if (waste(24) + 0.005 < waste(22)) c->tile_kind = 21;
+    }
     if (c->tile_kind <= 1) {  // small grids: the wide tiles cannot keep every SM busy -> 64x16, 2 CTAs/SM
         const TileShape t = tile_shape(c->tile_kind);
         const int64_t tiles = ((c->nx + t.tx - 1) / t.tx) * ((c->ny + t.ty - 1) / t.ty) * nl;
