@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -1
+python scripts/sweep.py "J3D_LIB=libjacobi3d_old.so" "J3D_X=0" "J3D_LIB=libjacobi3d_s0.so" "J3D_LIB=libjacobi3d_s100000.so" "--launch persistent" "J3D_LIB=libjacobi3d_s0.so --launch persistent" -- --workload fine384_odf64 --steps 200 --warmup 20
+python scripts/sweep.py "J3D_X=0" "J3D_LIB=libjacobi3d_s0.so" -- --workload weak1536_odf1 --steps 30 --warmup 5
+python scripts/sweep.py "J3D_X=0" "J3D_LIB=libjacobi3d_s0.so" "--launch persistent" -- --workload small192_odf1 --steps 500 --warmup 20
