@@ -186,7 +186,7 @@ struct jacobi3d {
     const unsigned int** d_remote_done = nullptr;      // every peer counter some slab waits for
     int n_remote_done = 0;
     unsigned int* d_done = nullptr;             // [n_slabs], in the arena at off_done
-    int n_slabs = 0, persist_nzc = 0;
+    int n_slabs = 0, persist_nzc = 0, persist_nty = 0;
     uint32_t slab_target = 0;                   // consumer warps x tiles per slab
     uint32_t persist_base = 0;                  // iterations counted in d_done (mod 2^32)
     int persist_n = 0;                          // set while launching a persistent stencil

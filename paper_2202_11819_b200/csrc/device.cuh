@@ -56,14 +56,14 @@ struct WorkItem {
 
 // Multi-iteration (persistent) stencil launches, J3D_PERSISTENT: launch item g
 // is item (g mod n_items) of relative iteration k = g / n_items.  A slab is
-// one block's tiles over one z chunk; done[s] counts consumer-warp completions
-// of slab s (mod 2^32, never reset).  An item of iteration k > 0 may start
-// once every slab in slab_deps[item_slab[i]] -- the slabs whose iteration-k-1
-// writes it reads (its own and the adjacent z chunks, the x/y neighbour
-// blocks' same chunk, the z neighbour's edge chunk) and, by symmetry, those
-// whose iteration-k-1 reads its writes would clobber -- has
-// done >= (base + k) * target.
-constexpr int MAX_DEPS = 9;
+// one row of tiles (all tx) of one block over one z chunk; done[s] counts
+// consumer-warp completions of slab s (mod 2^32, never reset).  An item of
+// iteration k > 0 may start once every slab in slab_deps[item_slab[i]] -- the
+// slabs whose iteration-k-1 writes it reads (own slab, the adjacent chunks
+// and tile rows, the x neighbours' same slab, the y / z neighbours' edge
+// slab; setup.cu build_persist_deps) and, by symmetry, those whose
+// iteration-k-1 reads its writes would clobber -- has done >= (base+k)*target.
+constexpr int MAX_DEPS = 12;
 constexpr int32_t SLAB_PEER = 1 << 30;      // item_slab flag: the slab touches a peer GPU's face
 constexpr int32_t SLAB_MASK = SLAB_PEER - 1;
 struct IterCtl {

@@ -27,7 +27,9 @@ void build_layout(jacobi3d* c) {
     // J3D_PERSISTENT slab completion counters (at most one slab per plane of each
     // local block); inside the arena so peers read them over NVLink
     c->off_done = 4096;
-    const int64_t done_bytes = c->cfg.launch == J3D_PERSISTENT ? (int64_t)c->n_local * c->nz * 4 : 0;
+    // one counter per (block, z chunk, tile row): chunks >= 1 plane, tile rows >= 8 rows
+    const int64_t done_bytes =
+        c->cfg.launch == J3D_PERSISTENT ? (int64_t)c->n_local * c->nz * ((c->ny + 7) / 8) * 4 : 0;
     c->off_bufs = align_up(c->off_done + done_bytes, 4096);
     c->off_faces = c->off_bufs + (int64_t)c->n_local * 2 * c->buf_bytes;
     c->arena_bytes = c->off_faces + (int64_t)c->n_local * c->faces_per_block_bytes;
@@ -238,44 +240,60 @@ void build_tables(jacobi3d* c) {
     build_persist_deps(c);
 }
 
-// J3D_PERSISTENT dependency tables (IterCtl, device.cuh).  The slabs an item
-// of slab (l, zc) waits for: its block's own and adjacent z chunks, the same
-// chunk of every x/y neighbour block, and for an edge chunk the z neighbour's
-// edge chunk it exchanges a ghost plane with.  A neighbour on a peer GPU is
-// named by a pointer into that rank's IPC-mapped arena (remote counters),
-// known only after jacobi3d_ipc_connect; `remote` collects those pointers for
-// the end-of-call wait.  The second table drops every remote entry (timing
-// with the exchange elided, jacobi3d_set_skip_exchange).
+// J3D_PERSISTENT dependency tables (IterCtl, device.cuh).  A slab is one row
+// of tiles (all tx) of one block over one z chunk: (l, zc, ty).  An item of
+// slab (l, zc, ty) reads, of the previous iteration's output, its own cells,
+// the boundary planes of chunks zc-1 / zc+1 and the boundary rows of tile
+// rows ty-1 / ty+1 (same block), the x ghost columns the x neighbours' slab
+// (zc, ty) wrote, for an edge tile row the y ghost row the y neighbour's edge
+// slab wrote, for an edge chunk the z ghost plane the z neighbour's edge slab
+// wrote -- and by symmetry of the 7-point neighbourhood exactly those slabs
+// read, in the previous iteration, the cells its own stores overwrite.
+// (Diagonal neighbours' corner cells are fetched by the TMA box but never
+// used.)  A neighbour on a peer GPU is named by a pointer into that rank's
+// IPC-mapped arena (remote counters), known only after jacobi3d_ipc_connect;
+// `remote` collects those pointers for the end-of-call wait.  The second
+// table drops every remote entry (timing with the exchange elided,
+// jacobi3d_set_skip_exchange).
 void build_persist_deps(jacobi3d* c) {
     if (c->cfg.launch != J3D_PERSISTENT) return;
-    const int nl = c->n_local, nzc = c->persist_nzc;
+    const int nl = c->n_local, nzc = c->persist_nzc, nty = c->persist_nty;
+    auto sid = [&](int l, int zc, int ty) { return ((int64_t)l * nzc + zc) * nty + ty; };
     std::vector<const unsigned int*> deps((size_t)c->n_slabs * MAX_DEPS, nullptr), local(deps);
     std::vector<const unsigned int*> remote;
-    auto counter = [&](int l, int f, int zc) -> const unsigned int* {
-        if (c->kind[l][f] == LOCAL) return c->d_done + c->nbr_local[l][f] * nzc + zc;
+    // counter of slab (zc, ty) of the neighbour across face f of block l
+    auto counter = [&](int l, int f, int zc, int ty) -> const unsigned int* {
+        if (c->kind[l][f] == LOCAL) return c->d_done + sid(c->nbr_local[l][f], zc, ty);
         if (c->kind[l][f] != PEER_P2P || !c->p2p_connected) return nullptr;
         const int r = c->plan.blocks[c->plan.blocks[c->gid[l]].nbr[f]].owner;
-        const uintptr_t p = (uintptr_t)((const unsigned int*)(c->peer_base[r] + c->off_done) + c->nbr_local[l][f] * nzc + zc);
+        const uintptr_t p = (uintptr_t)((const unsigned int*)(c->peer_base[r] + c->off_done) +
+                                        sid(c->nbr_local[l][f], zc, ty));
         return (const unsigned int*)(p | 1);  // tag: system-scope acquire (device.cuh)
     };
     for (int l = 0; l < nl; ++l)
-        for (int zc = 0; zc < nzc; ++zc) {
-            const unsigned int** d = &deps[(size_t)(l * nzc + zc) * MAX_DEPS];
-            const unsigned int** dl = &local[(size_t)(l * nzc + zc) * MAX_DEPS];
-            int n = 0, nloc = 0;
-            auto add = [&](const unsigned int* p, bool is_local) {
-                if (!p) return;
-                if (n == MAX_DEPS) throw Error(J3D_EUNSUPPORTED, "slab dependency table overflow");
-                d[n++] = p;
-                if (is_local) dl[nloc++] = p;
-                else if (std::find(remote.begin(), remote.end(), p) == remote.end()) remote.push_back(p);
-            };
-            for (int dz = -1; dz <= 1; ++dz)
-                if (zc + dz >= 0 && zc + dz < nzc) add(c->d_done + l * nzc + zc + dz, true);
-            for (int f = 0; f < 4; ++f) add(counter(l, f, zc), c->kind[l][f] == LOCAL);
-            if (zc == 0) add(counter(l, 4, nzc - 1), c->kind[l][4] == LOCAL);
-            if (zc == nzc - 1) add(counter(l, 5, 0), c->kind[l][5] == LOCAL);
-        }
+        for (int zc = 0; zc < nzc; ++zc)
+            for (int ty = 0; ty < nty; ++ty) {
+                const unsigned int** d = &deps[(size_t)sid(l, zc, ty) * MAX_DEPS];
+                const unsigned int** dl = &local[(size_t)sid(l, zc, ty) * MAX_DEPS];
+                int n = 0, nloc = 0;
+                auto add = [&](const unsigned int* p, bool is_local) {
+                    if (!p) return;
+                    if (n == MAX_DEPS) throw Error(J3D_EUNSUPPORTED, "slab dependency table overflow");
+                    d[n++] = p;
+                    if (is_local) dl[nloc++] = p;
+                    else if (std::find(remote.begin(), remote.end(), p) == remote.end()) remote.push_back(p);
+                };
+                add(c->d_done + sid(l, zc, ty), true);
+                if (zc > 0) add(c->d_done + sid(l, zc - 1, ty), true);
+                if (zc + 1 < nzc) add(c->d_done + sid(l, zc + 1, ty), true);
+                if (ty > 0) add(c->d_done + sid(l, zc, ty - 1), true);
+                if (ty + 1 < nty) add(c->d_done + sid(l, zc, ty + 1), true);
+                for (int f = 0; f < 2; ++f) add(counter(l, f, zc, ty), c->kind[l][f] == LOCAL);
+                if (ty == 0) add(counter(l, 2, zc, nty - 1), c->kind[l][2] == LOCAL);
+                if (ty == nty - 1) add(counter(l, 3, zc, 0), c->kind[l][3] == LOCAL);
+                if (zc == 0) add(counter(l, 4, nzc - 1, ty), c->kind[l][4] == LOCAL);
+                if (zc == nzc - 1) add(counter(l, 5, 0, ty), c->kind[l][5] == LOCAL);
+            }
     for (auto& p : remote) p = (const unsigned int*)((uintptr_t)p & ~uintptr_t(1));
     CK(cudaMemcpy(c->d_slab_deps, deps.data(), deps.size() * sizeof(void*), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->d_slab_deps_local, local.data(), local.size() * sizeof(void*), cudaMemcpyHostToDevice));
@@ -433,18 +451,18 @@ void build_static_tables(jacobi3d* c) {
         // persistent: slabs that wait on a peer LAST -- the peer's matching slabs
         // were the last of its previous iteration too, so a GPU may run up to an
         // iteration ahead of a slower neighbour instead of meeting it at every
-        // iteration start.  Whole slabs move (a slab completes only with all its
-        // tiles, so splitting one would delay every dependant of it).
-        std::vector<uint8_t> ext_slab((size_t)nl * best_zc, 0);
+        // iteration start.  Whole slabs (tile rows) move: a slab completes only
+        // with all its tiles, so splitting one would delay every dependant of it.
         auto zc_of = [&](const WorkItem& w) {
             int zc = 0;
             while ((int)(c->nz * (zc + 1) / best_zc) <= w.z0) ++zc;
             return zc;
         };
+        std::vector<uint8_t> ext_slab((size_t)nl * best_zc * nty, 0);
+        auto row_slab = [&](const WorkItem& w) { return ((size_t)w.blk * best_zc + zc_of(w)) * nty + w.ty; };
         for (const WorkItem& w : items)
-            if (exterior(w)) ext_slab[(size_t)w.blk * best_zc + zc_of(w)] = 1;
-        std::stable_partition(items.begin(), items.end(),
-                              [&](const WorkItem& w) { return !ext_slab[(size_t)w.blk * best_zc + zc_of(w)]; });
+            if (exterior(w)) ext_slab[row_slab(w)] = 1;
+        std::stable_partition(items.begin(), items.end(), [&](const WorkItem& w) { return !ext_slab[row_slab(w)]; });
     }
     c->n_items = (int)items.size();
     c->item_cells.assign(items.size() + 1, 0);
@@ -455,24 +473,26 @@ void build_static_tables(jacobi3d* c) {
         c->item_cells[i + 1] = c->item_cells[i] + ex * ey * (w.z1 - w.z0);
     }
     if (c->cfg.launch == J3D_PERSISTENT) {
-        // slab = (local block, z chunk); the dependency tables are built by build_persist_deps
+        // slab = (local block, z chunk, tile row); the dependency tables are built by
+        // build_persist_deps
         const int nzc = (int)best_zc;
-        if (nzc > c->nz) throw Error(J3D_EUNSUPPORTED, "more z chunks than planes");
         c->persist_nzc = nzc;
-        c->n_slabs = nl * nzc;
-        c->slab_target = (uint32_t)(ts.ncw * ntx * nty);
+        c->persist_nty = (int)nty;
+        c->n_slabs = nl * nzc * (int)nty;
+        if ((int64_t)c->n_slabs * 4 > c->off_bufs - c->off_done)
+            throw Error(J3D_EUNSUPPORTED, "persistent slab counters exceed their arena region");
+        c->slab_target = (uint32_t)(ts.ncw * ntx);
         std::vector<int32_t> slab(items.size());
         for (size_t i = 0; i < items.size(); ++i) {
             const WorkItem& w = items[i];
             int zc = 0;
             while ((int)(c->nz * (zc + 1) / best_zc) <= w.z0) ++zc;
-            // slab flag SLAB_PEER: some item of the slab touches a peer face
-            bool peer = false;
-            for (int f = 0; f < 6 && !peer; ++f) {
-                if (!is_peer(w.blk, f)) continue;
-                peer = f < 4 || (f == 4 && zc == 0) || (f == 5 && zc == nzc - 1);
-            }
-            slab[i] = (w.blk * nzc + zc) | (peer ? SLAB_PEER : 0);
+            // slab flag SLAB_PEER: some item of the slab touches a peer face (its
+            // stores reach the peer; the peer reads its counter over NVLink)
+            const bool peer = is_peer(w.blk, 0) || is_peer(w.blk, 1) || (is_peer(w.blk, 2) && w.ty == 0) ||
+                              (is_peer(w.blk, 3) && w.ty == nty - 1) || (is_peer(w.blk, 4) && zc == 0) ||
+                              (is_peer(w.blk, 5) && zc == nzc - 1);
+            slab[i] = (int32_t)(((int64_t)w.blk * nzc + zc) * nty + w.ty) | (peer ? SLAB_PEER : 0);
         }
         CK(cudaMalloc(&c->d_item_slab, std::max<size_t>(1, slab.size()) * sizeof(int32_t)));
         CK(cudaMemcpy(c->d_item_slab, slab.data(), slab.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
