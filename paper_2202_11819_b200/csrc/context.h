@@ -175,7 +175,7 @@ struct jacobi3d {
     unsigned int* d_sched = nullptr;            // [2*(n_local+1)] stencil work counters
     bool peer_x_pack = true;     // peer x faces packed from the output by the push kernel (J3D_PEERX_PACK=0:
                                  // captured by the stencil epilogue into the send buffer; tuning)
-    bool peer_x_direct = false;  // J3D_PEERX_DIRECT=1: peer x ghosts stored over NVLink from the epilogue (tuning)  // J3D_XSECTOR=0 disables whole-sector x-ghost stores (tuning)
+    bool peer_x_direct = false;  // J3D_PEERX_DIRECT=1: peer x ghosts stored over NVLink from the epilogue (tuning)
     std::vector<int> item_begin, item_count;  // per local block, in d_items
     std::vector<int64_t> item_cells;          // prefix sums of owned cells per item (profiling bytes)
     int n_items = 0, tile_kind = 0, grid_cap = 0;
