@@ -14,16 +14,19 @@
 //
 // Stencil design: HBM-bound (16 B per lattice-site
 // update, 0.44 flop/B), so no tensor cores.  A persistent grid of CTAs walks
-// a list of work items (block, xy tile, z range).  Per CTA one producer warp
-// streams (TX+4) x (TY+2) xy-planes of the input buffer -- the tile plus its
-// 1-cell halo, ghost cells included -- into an NSTAGE-deep shared-memory ring
-// with TMA (cp.async.bulk.tensor.3d, mbarrier complete_tx).  Eight consumer
-// warps march up z: each thread keeps the centre values of planes z-1, z,
-// z+1 for its 2*CPL x RPW cells in registers, reads the four in-plane
-// neighbours of plane z from shared memory, and writes 16-byte vector stores
-// of the new plane to HBM.  Every input plane is fetched once per tile (plus
-// the 1-cell halo, which neighbouring tiles fetch concurrently and therefore
-// hit in L2), every output cell written once: the compulsory 16 B/LUP.
+// a list of work items (block, xy tile, z range) -- for J3D_PERSISTENT, n
+// iterations of that list, with per-slab completion counters ordering the
+// iterations.  Per CTA one producer warp streams (TX+8) x (TY+2) xy-planes of
+// the input buffer -- the tile plus its 1-cell halo, y/z ghost rows included,
+// x ghost values from the separate x ghost arrays for tiles at a block x
+// edge -- into an NSTAGE-deep shared-memory ring with TMA
+// (cp.async.bulk.tensor.3d, mbarrier complete_tx).  NCW consumer warps march
+// up z holding the stages of planes z-1, z, z+1, read all seven inputs of a
+// cell from shared memory and write the new plane to HBM (16-byte vector
+// stores for the cell-pair lane map).  Every input plane is fetched once per
+// tile (plus the halo, which neighbouring tiles fetch concurrently and
+// therefore mostly hit in L2), every output cell written once: the
+// compulsory 16 B/LUP.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
