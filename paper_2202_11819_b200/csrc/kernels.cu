@@ -273,15 +273,20 @@ __device__ __forceinline__ void patch_stage(const StencilDesc* __restrict__ d, d
     if (lane < T::RPW) {
         const int y = y0 + r0 + lane;
         if (y < ny) {
+            // the -x / +x ghost of the row: its halo column (cell-pair map) or its
+            // entry of the stage's x ghost vector (one-cell map reads it there)
             if ((pro & 1u) && x0 == 0) {
                 const FaceRef F = load_face(&d->pro[0]);
-                st[(r0 + lane + 1) * W + T::HX - 1] = F.p[y * F.sa + zz * F.sb];
+                const int i = T::MAP == 1 ? T::SIDE_OFF / 8 + r0 + lane : (r0 + lane + 1) * W + T::HX - 1;
+                st[i] = F.p[y * F.sa + zz * F.sb];
             }
             if (pro & 2u) {
                 const int gx = nx - x0;  // tile-local x of the +x ghost
-                if (gx <= T::TX + 1) {
+                if (gx <= T::TX) {
                     const FaceRef F = load_face(&d->pro[1]);
-                    st[(r0 + lane + 1) * W + gx + T::HX] = F.p[y * F.sa + zz * F.sb];
+                    const int i = T::MAP == 1 ? (T::SIDE_OFF + T::SIDE_STRIDE) / 8 + r0 + lane
+                                              : (r0 + lane + 1) * W + gx + T::HX;
+                    st[i] = F.p[y * F.sa + zz * F.sb];
                 }
             }
         }
@@ -471,9 +476,16 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
         const int edl = (er + 1) * W + T::HX - 1, esl = T::SIDE_OFF / 8 + er;
         const int edr = (er + 1) * W + T::HX + (nx - x0), esr = (T::SIDE_OFF + T::SIDE_STRIDE) / 8 + er;
         const bool ecopy = (touch & 3u) && lane < RPW;
+        // MAP 1 reads the x ghost vectors in place instead (xlb / xrb: offsets of
+        // this thread's row-0 vector entries from its edge cell; see compute_plane_s)
+        const int xlast_t = nx - 1 - x0, kedge = xlast_t >> 5;
+        const bool xlf = (touch & 1u) && lane == 0;
+        const bool xrf = (touch & 2u) && lane == (xlast_t & 31);
+        const int xlb = T::SIDE_OFF / 8 + warp * RPW - sbase;
+        const int xrb = (T::SIDE_OFF + T::SIDE_STRIDE) / 8 + warp * RPW - sbase - 32 * kedge;
         auto acquire = [&](int zz) {
             mbar_wait(&full[s], ph);
-            if (touch & 3u) {
+            if (T::MAP == 0 && (touch & 3u)) {
                 if (ecopy) {
                     double* st = stage(s);
                     if (touch & 1u) st[edl] = st[esl];
@@ -691,7 +703,11 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                 for (int k = 0; k < KPL; ++k) {
                     const int off = r * W + 32 * k;
                     const double* p = pc + off;
-                    const double sv = sum7(p[0], p[-1], p[1], p[-W], p[W], pm[off], pp[off]);
+                    // block x edge: the neighbour outside the block comes from the
+                    // stage's x ghost vector (offsets fixed for the item)
+                    const int om = (k == 0 && xlf) ? xlb + r * (1 - W) : -1;
+                    const int oq = (k == kedge && xrf) ? xrb + r * (1 - W) : 1;
+                    const double sv = sum7(p[0], p[om], p[oq], p[-W], p[W], pm[off], pp[off]);
                     tiny |= fabs(sv) < kDiv7Tiny;
                     const double v = div7_fast(sv);
                     if constexpr (MODE >= 1) {
@@ -741,7 +757,9 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                         if (y >= ny || x >= nx) continue;
                         const int off = r * W + 32 * k;
                         const double* p = pc + off;
-                        const double v = div7(sum7(p[0], p[-1], p[1], p[-W], p[W], pm[off], pp[off]));
+                        const int om = (k == 0 && xlf) ? xlb + r * (1 - W) : -1;
+                        const int oq = (k == kedge && xrf) ? xrb + r * (1 - W) : 1;
+                        const double v = div7(sum7(p[0], p[om], p[oq], p[-W], p[W], pm[off], pp[off]));
                         op[r * pitch + 32 * k] = v;
                         const uint32_t m = tiny ? fm : (rare_faces & fm);
                         // epi_store writes pairs; pass (v, v) with has2 = false
