@@ -43,13 +43,16 @@ def _check(ctx, grid, n, rng):
         assert np.float64(got).tobytes() == np.float64(want).tobytes(), ((i, j, k), got, want)
 
 
-@pytest.mark.parametrize("odf,variant", [(1, "direct"), (8, "direct"), (8, "unfused"), (8, "C")])
-def test_weak_1536_sampled(odf, variant):
+@pytest.mark.parametrize("odf,variant,launch", [(1, "direct", "batched"), (8, "direct", "batched"),
+                                               (8, "unfused", "batched"), (8, "C", "batched"),
+                                               (1, "direct", "persistent"), (8, "direct", "persistent")])
+def test_weak_1536_sampled(odf, variant, launch):
     """configs[1]/[2]: 1536^3 per GPU, ODF 1 and 8, hash-random interior (seed
-    20220223), 3 iterations, batched launch (bench.py's configuration)."""
+    20220223), 3 iterations, batched launch (bench.py's configuration) and the
+    persistent launch (3 iterations in one kernel)."""
     grid = (1536, 1536, 1536)
     rng = np.random.default_rng(odf)
-    with j3d.Jacobi3D(grid, odf=odf, variant=variant, launch="batched") as ctx:
+    with j3d.Jacobi3D(grid, odf=odf, variant=variant, launch=launch) as ctx:
         ctx.init("hash", seed=SEED)
         ctx.iterate(3)
         ctx.synchronize()
