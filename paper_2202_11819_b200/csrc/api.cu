@@ -75,10 +75,15 @@ int jacobi3d_plan(const jacobi3d_config* cfg, jacobi3d_plan_info* out) {
         // bytes: same layout as build_layout
         const int64_t nx = P.ext[0], ny = P.ext[1], nz = P.ext[2];
         const int64_t pitch = align_up(XOFF + nx + 1, PITCH_ALIGN);
-        const int64_t buf = align_up(pitch * (ny + 2) * (nz + 2) * 8, 256);
+        const int64_t grid = align_up(pitch * (ny + 2) * (nz + 2) * 8, 256);
+        const int64_t xg = align_up(align_up(ny, 2) * (nz + 2) * 8, 256);  // two x ghost arrays per buffer
+        const int64_t buf = grid + 2 * xg;
         int64_t faces = 0;
         for (int f = 0; f < 6; ++f) faces += 4 * align_up(face_cells(P.ext, f) * 8, 256);
-        out->bytes_per_gpu = 4096 + (int64_t)P.odf * (2 * buf + faces);
+        const int64_t head = cfg->launch == J3D_PERSISTENT
+                                 ? align_up(4096 + (int64_t)P.odf * nz * ((ny + 7) / 8) * 4, 4096)
+                                 : 4096;
+        out->bytes_per_gpu = head + (int64_t)P.odf * (2 * buf + faces);
         int32_t pmax = 0;
         for (int r = 0; r < P.n_gpus; ++r) {
             int32_t cnt = 0, loc = 0;

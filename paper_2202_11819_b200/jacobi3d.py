@@ -115,9 +115,9 @@ def make_config(grid, odf=1, n_gpus=1, rank=0, device=0, block=(0, 0, 0), varian
                   boundary)
 
 
-def plan(grid, odf=1, n_gpus=1, block=(0, 0, 0), rank=0) -> dict:
+def plan(grid, odf=1, n_gpus=1, block=(0, 0, 0), rank=0, launch="batched") -> dict:
     """jacobi3d_plan: decomposition without a GPU."""
-    cfg = make_config(grid, odf=odf, n_gpus=n_gpus, rank=rank, block=block)
+    cfg = make_config(grid, odf=odf, n_gpus=n_gpus, rank=rank, block=block, launch=launch)
     info = PlanInfo()
     _ck(lib.jacobi3d_plan(ctypes.byref(cfg), ctypes.byref(info)))
     return {"gpu_grid": tuple(info.gpu_grid), "blk_grid": tuple(info.blk_grid), "blk_ext": tuple(info.blk_ext),

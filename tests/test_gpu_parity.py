@@ -227,3 +227,16 @@ def test_every_tile_kind(kind, monkeypatch):
     _case((200, 45, 30), 2, "direct", "batched", False, 6, kind="hash", seed=kind + 1)
     _case((96, 40, 24), 8, "C", "batched", False, 5, kind="hash", seed=kind + 2)
     _case((45, 34, 22), 2, "unfused", "batched", False, 5, kind="hash", seed=kind + 3)
+
+
+@pytest.mark.parametrize("grid,odf,launch", [((64, 64, 64), 8, "batched"), ((45, 34, 22), 2, "batched"),
+                                             ((96, 96, 96), 8, "persistent"), ((200, 40, 30), 1, "persistent")])
+def test_plan_bytes_match_allocation(grid, odf, launch):
+    """jacobi3d_plan's bytes_per_gpu (no GPU) equals the arena the context
+    allocates (x ghost arrays, persistent counters and face buffers included)."""
+    import struct
+
+    want = j3d.plan(grid, odf=odf, launch=launch)["bytes_per_gpu"]
+    with j3d.Jacobi3D(grid, odf=odf, variant="direct", launch=launch) as ctx:
+        rec = ctx.ipc_export()
+    assert struct.unpack_from("<Q", rec, 16)[0] == want
