@@ -45,11 +45,11 @@ WORKLOADS = {
     # SURVEY 8(d) config 4': strong scaling that reaches 1 GPU, 1536^3 global, ODF 8
     "strong1536_odf8": dict(kind="strong", global_=(1536, 1536, 1536), odf=8),
     # configs[4]: fine-grained, 768^3 global (8 GPUs x ODF 64 = 96^3 blocks)
-    "fine768_odf64": dict(kind="strong", global_=(768, 768, 768), odf=64),
+    "fine768_odf64": dict(kind="strong", global_=(768, 768, 768), odf=64, launch="persistent"),
     # configs[4] per GPU: 384^3 per GPU with ODF 64 = the 96^3 blocks of 768^3 on 8 GPUs
-    "fine384_odf64": dict(kind="weak", per_gpu=(384, 384, 384), odf=64),
+    "fine384_odf64": dict(kind="weak", per_gpu=(384, 384, 384), odf=64, launch="persistent"),
     # the paper's small weak-scaling problem (192^3 per node)
-    "small192_odf1": dict(kind="weak", per_gpu=(192, 192, 192), odf=1),
+    "small192_odf1": dict(kind="weak", per_gpu=(192, 192, 192), odf=1, launch="persistent"),
     # configs[0]: the small oracle-checkable case
     "small64_odf8": dict(kind="strong", global_=(64, 64, 64), odf=8),
 }
@@ -187,7 +187,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="weak1536_odf1", choices=sorted(WORKLOADS))
     ap.add_argument("--variant", default="direct")
-    ap.add_argument("--launch", default="batched")
+    ap.add_argument("--launch", default=None,
+                    help="per_block | batched | persistent (default: the workload's measured best; "
+                         "batched for the 1536^3 configs, persistent for the small / fine-grained ones)")
     ap.add_argument("--graph", type=int, default=0)
     ap.add_argument("--exchange", default="auto")
     ap.add_argument("--overlap", type=int, default=0)
@@ -214,6 +216,8 @@ def main():
     if a.grid:
         grid = tuple(int(x) for x in a.grid.split(","))
     odf = a.odf or wl["odf"]
+    if a.launch is None:  # the persistent launch exists for the direct variant only
+        a.launch = wl.get("launch", "batched") if a.variant == "direct" else "batched"
     cfg_json = {"workload": a.workload, "grid": list(grid), "odf": odf, "variant": a.variant, "launch": a.launch,
                 "graph": bool(a.graph), "exchange": a.exchange, "overlap": bool(a.overlap), "n_gpus": n,
                 "l2": "inputs larger than L2 (no flush needed)" if grid[0] * grid[1] * grid[2] * 16 / n > L2_BYTES
