@@ -28,3 +28,19 @@ def test_warmup_must_be_at_least_three():
     p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
                         "--warmup", "1"], capture_output=True, text=True, timeout=120)
     assert p.returncode != 0
+
+
+def test_workload_launch_defaults_in_config():
+    """The reference arm reports the same config as the GPU arm, including the
+    launch mode each workload defaults to (persistent for the small and
+    fine-grained grids, batched for the 1536^3 ones and for non-direct variants)."""
+    def cfg(*args):
+        p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "3",
+                            "--warmup", "3", *args], capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stderr
+        return json.loads([l for l in p.stdout.splitlines() if l.startswith("{")][-1])["config"]
+
+    assert cfg("--workload", "small64_odf8")["launch"] == "batched"
+    assert cfg("--workload", "small192_odf1", "--grid", "64,64,32")["launch"] == "persistent"
+    assert cfg("--workload", "small192_odf1", "--grid", "64,64,32", "--variant", "unfused")["launch"] == "batched"
+    assert cfg("--workload", "small192_odf1", "--grid", "64,64,32", "--launch", "per_block")["launch"] == "per_block"
