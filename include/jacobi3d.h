@@ -252,7 +252,10 @@ J3D_API int jacobi3d_set_skip_exchange(jacobi3d_t *ctx, int skip);
  * first failing s, kernel result, IEEE result. */
 J3D_API int jacobi3d_div7_selftest(uint64_t n, uint64_t seed, uint64_t *mismatches, double *example);
 
-/* Free everything.  NULL-safe.  Collective when n_gpus > 1. */
+/* Free everything.  NULL-safe.  Collective when n_gpus > 1: it begins with a
+ * barrier over the context's communicator, so no peer can still read (persistent
+ * launch: slab counters) or write (epilogue / pack stores) this rank's memory
+ * when it is freed. */
 J3D_API int jacobi3d_destroy(jacobi3d_t *ctx);
 
 /* Message of the last failing call on this thread ("" if none). */

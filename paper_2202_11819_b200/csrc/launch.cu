@@ -310,6 +310,17 @@ void destroy_ctx(jacobi3d* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
+    // collective (jacobi3d.h): once every rank is here no peer still touches this
+    // rank's arena -- persistent launches read the peers' slab counters over NVLink
+    // until their own last iteration -- so freeing it cannot fault a slower peer
+    bool abort_comm = false;
+    if (c->n_gpus > 1 && c->comm) {
+        try {
+            nccl_barrier(c);
+        } catch (...) {
+            abort_comm = true;
+        }
+    }
     drop_graphs(c);
     for (auto& pr : c->prof_events) {
         cudaEventDestroy(pr.first);
@@ -328,7 +339,10 @@ void destroy_ctx(jacobi3d* c) {
     if (c->ev_t1) cudaEventDestroy(c->ev_t1);
     for (auto s : c->lo) if (s) cudaStreamDestroy(s);
     for (auto s : c->hi) if (s) cudaStreamDestroy(s);
-    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->comm) {
+        if (abort_comm) ncclCommAbort(c->comm);
+        else ncclCommDestroy(c->comm);
+    }
     for (size_t r = 0; r < c->peer_base.size(); ++r)
         if (c->peer_base[r]) cudaIpcCloseMemHandle(c->peer_base[r]);
     host_teardown(c);

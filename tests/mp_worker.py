@@ -127,6 +127,24 @@ def run_set_block_case(grid, odf, variant, exchange, launch="batched"):
         ctx.close()
 
 
+def run_destroy_race(grid):
+    """Persistent launch, ranks deliberately skewed, destroy right after iterate
+    (no collective in between): destroy's barrier must keep the faster rank's
+    arena alive while the slower rank still polls its counters; a fresh context
+    afterwards must give the oracle's bits."""
+    import time
+
+    rank = dist.get_rank()
+    ctx = jdist.create(grid, odf=2, variant="direct", launch="persistent", exchange="p2p")
+    ctx.init("hash", seed=3)
+    dist.barrier()
+    if rank == 1:
+        time.sleep(1.5)
+    ctx.iterate(40)
+    ctx.close()
+    run_case(grid, 2, "direct", "persistent", False, "p2p", 5, "hash", 4)
+
+
 def run_api_case(grid):
     """Rank-local API errors and the epoch-wait watchdog on a multi-GPU context:
     get_block of a block owned by another rank -> J3D_ENOTLOCAL; a rank whose
@@ -223,6 +241,7 @@ def main():
         cases = [c for c in cases if c[0] == gx]
     if which == "persistent":
         cases = [c for c in cases if c[3] == "persistent"]
+        run_destroy_race(g)
         for zc in ("1", "3"):  # many thin slabs: long dependency chains across GPUs
             os.environ["J3D_ZCHUNK"] = zc
             try:
@@ -237,6 +256,12 @@ def main():
     if which not in ("debug", "xsplit", "persistent"):
         try:
             run_api_case(g)
+        except AssertionError as e:
+            failed.append(str(e))
+            print("FAIL", e, flush=True)
+        n += 1
+        try:
+            run_destroy_race(g)
         except AssertionError as e:
             failed.append(str(e))
             print("FAIL", e, flush=True)
