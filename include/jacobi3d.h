@@ -134,8 +134,9 @@ typedef struct {          /* filled by jacobi3d_plan: integers only, no GPU need
     int64_t blk_ext[3];   /* block extent (bx,by,bz)                                             */
     int64_t n_blocks;     /* odf * n_gpus; block id = x-fastest linear index on the global block
                              grid (gpu_grid * blk_grid)                                          */
-    int64_t bytes_per_gpu;/* device bytes one rank allocates (2 ghosted buffers per block, row
-                             pitch padding, face buffers x 2 parities, flags)                    */
+    int64_t bytes_per_gpu;/* device bytes one rank allocates (2 ghosted buffers per block incl.
+                             their x ghost arrays and row pitch padding, face buffers x 2
+                             parities, flags, persistent-launch counters)                         */
     int32_t peer_faces_max; /* max over ranks of block faces whose neighbour is on another GPU  */
     int32_t local_faces;    /* block faces (this rank, rank 0 if plan-only) with a same-GPU nbr */
 } jacobi3d_plan_info;
@@ -192,7 +193,10 @@ J3D_API int jacobi3d_set_block(jacobi3d_t *ctx, int64_t block_id, const double *
 J3D_API int jacobi3d_refresh_halos(jacobi3d_t *ctx);
 
 /* Enqueue n Jacobi iterations on the context's streams.  Asynchronous: it
- * returns once the work is queued; no host synchronisation per iteration. */
+ * returns once the work is queued; no host synchronisation per iteration.
+ * J3D_PERSISTENT: one stencil launch for all n (plus, across GPUs, one small
+ * end-of-call wait kernel).  J3D_ESTATE if halos are stale on a multi-GPU
+ * context or P2P peers are not connected.  n = 0 enqueues nothing. */
 J3D_API int jacobi3d_iterate(jacobi3d_t *ctx, int64_t n);
 
 /* Wait for all queued work; surfaces deferred CUDA / NCCL errors. */
@@ -227,6 +231,7 @@ J3D_API int jacobi3d_checksum(jacobi3d_t *ctx, uint64_t *out);
  * events on the context's main stream (after a device synchronize and, for
  * n_gpus > 1, a barrier).  *ms_per_iter = this rank's elapsed / iters. */
 J3D_API int jacobi3d_time(jacobi3d_t *ctx, int64_t warmup, int64_t iters, double *ms_per_iter);
+/* (J3D_PERSISTENT: the timed iters iterations are one launch.) */
 
 /* Stats / launch counters (SPEC.md L424 launch-count law). */
 J3D_API int jacobi3d_get_stats(jacobi3d_t *ctx, jacobi3d_stats *out);
