@@ -74,6 +74,7 @@ struct IterCtl {
     uint32_t target;                        // completions per slab per iteration (consumer warps x tiles per slab)
     uint32_t base;                          // iterations counted in done[] before this launch
     int32_t sys;                            // 1: some slabs wait on peer counters (iteration 0 waits too)
+    uint64_t timeout_ns;                    // a counter wait longer than this traps (J3D_TIMEOUT_S)
 };
 
 // A strided 2D face copy (pack: owned layer -> send buffer / peer receive

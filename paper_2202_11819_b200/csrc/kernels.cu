@@ -86,14 +86,15 @@ __device__ __forceinline__ uint64_t global_ns() {
 
 // Persistent launches: wait until the slabs item `it` depends on have
 // finished `iters` iterations (IterCtl, device.cuh), then order the async
-// proxy (TMA) after the acquired generic-proxy writes.  A wait beyond 60 s
-// can only be a bug: trap rather than hang the GPU.
-__device__ __forceinline__ void wait_counter(const unsigned int* p, uint32_t need, bool sys) {
+// proxy (TMA) after the acquired generic-proxy writes.  A wait beyond the
+// context's limit (J3D_TIMEOUT_S) means a peer stopped or a bug: trap rather
+// than hang the GPU.
+__device__ __forceinline__ void wait_counter(const unsigned int* p, uint32_t need, bool sys, uint64_t limit_ns) {
     if ((int32_t)(ld_acquire_u32(p, sys) - need) >= 0) return;
     const uint64_t t0 = global_ns();
     while ((int32_t)(ld_acquire_u32(p, sys) - need) < 0) {
         __nanosleep(128);
-        if (global_ns() - t0 > 60ull * 1000000000ull) __trap();
+        if (global_ns() - t0 > limit_ns) __trap();
     }
 }
 
@@ -104,7 +105,7 @@ __device__ __noinline__ void wait_slabs(const IterCtl ctl, int it, uint32_t iter
         const uintptr_t p = reinterpret_cast<uintptr_t>(dp[j]);
         if (!p) break;
         // bit 0 tags a peer GPU's counter: acquire at system scope
-        wait_counter(reinterpret_cast<const unsigned int*>(p & ~uintptr_t(1)), need, (p & 1) != 0);
+        wait_counter(reinterpret_cast<const unsigned int*>(p & ~uintptr_t(1)), need, (p & 1) != 0, ctl.timeout_ns);
     }
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -825,8 +826,8 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
 // the peers' epilogue stores into this GPU's ghost layers for the call's
 // iterations have all landed when this kernel completes.
 __global__ void __launch_bounds__(32) wait_counters_kernel(const unsigned int* const* __restrict__ ptrs, int n,
-                                                          uint32_t need) {
-    for (int i = threadIdx.x; i < n; i += 32) wait_counter(ptrs[i], need, true);
+                                                          uint32_t need, uint64_t limit_ns) {
+    for (int i = threadIdx.x; i < n; i += 32) wait_counter(ptrs[i], need, true, limit_ns);
     __threadfence_system();
 }
 
@@ -1048,9 +1049,10 @@ cudaError_t stencil_occupancy(int kind, bool, int* blocks_per_sm) {
 int stencil_box_w(int kind) { return tile_shape(kind).tx + 8; }
 int stencil_box_h(int kind) { return tile_shape(kind).ty + 2; }
 
-cudaError_t launch_wait_counters(const unsigned int* const* ptrs, int n, uint32_t need, cudaStream_t st) {
+cudaError_t launch_wait_counters(const unsigned int* const* ptrs, int n, uint32_t need, uint64_t limit_ns,
+                                 cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
-    wait_counters_kernel<<<1, 32, 0, st>>>(ptrs, n, need);
+    wait_counters_kernel<<<1, 32, 0, st>>>(ptrs, n, need, limit_ns);
     return cudaGetLastError();
 }
 

@@ -38,7 +38,8 @@ cudaError_t launch_stencil(const StencilLaunch& L, cudaStream_t st);
 cudaError_t stencil_occupancy(int kind, bool faces, int* blocks_per_sm);
 cudaError_t launch_div7_selftest(uint64_t n, uint64_t seed, unsigned long long* bad, double* example, int sms,
                                  cudaStream_t st);
-cudaError_t launch_wait_counters(const unsigned int* const* ptrs, int n, uint32_t need, cudaStream_t st);
+cudaError_t launch_wait_counters(const unsigned int* const* ptrs, int n, uint32_t need, uint64_t limit_ns,
+                                 cudaStream_t st);
 cudaError_t launch_copy_faces(const CopyDesc* d, int per_group, int groups, int64_t max_cells, cudaStream_t st);
 cudaError_t launch_init(const BlockGeom* g, int nblocks, int max_nx, int64_t max_rows, int kind, const double* p,
                         uint64_t seed, double boundary, int64_t gx, int64_t gy, int64_t gz, cudaStream_t st);

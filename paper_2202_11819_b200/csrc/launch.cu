@@ -27,6 +27,16 @@ void count_launch(jacobi3d* c, int l) {
     }
 }
 
+// Limit for the persistent launch's on-device counter waits: the host-wait
+// watchdog's J3D_TIMEOUT_S (default 600 s), so a legitimately late peer rank
+// is waited for as long as the host would wait for it.
+static uint64_t wait_limit_ns() {
+    double s = 600.0;
+    if (const char* e = std::getenv("J3D_TIMEOUT_S")) s = std::atof(e);
+    if (!(s > 0)) s = 600.0;
+    return (uint64_t)(s * 1e9);
+}
+
 void stencil(jacobi3d* c, int begin, int count, int parity, cudaStream_t st, int l) {
     if (count <= 0) return;
     StencilLaunch L;
@@ -42,12 +52,12 @@ void stencil(jacobi3d* c, int begin, int count, int parity, cudaStream_t st, int
     L.kind = c->tile_kind;
     L.faces = c->faces_fused;
     L.sched = c->d_sched + 2 * (l + 1);  // one counter pair per concurrently running launch
-    L.ctl = IterCtl{nullptr, nullptr, nullptr, 1, 0, 0, 0};
+    L.ctl = IterCtl{nullptr, nullptr, nullptr, 1, 0, 0, 0, 0};
     const int n_iter = c->persist_n;
     if (n_iter > 0) {  // J3D_PERSISTENT: n_iter iterations in this one launch
         const bool remote = c->n_remote_done > 0 && !c->skip_exchange;
         L.ctl = IterCtl{c->d_item_slab, remote ? c->d_slab_deps : c->d_slab_deps_local, c->d_done, n_iter,
-                        c->slab_target, c->persist_base, remote ? 1 : 0};
+                        c->slab_target, c->persist_base, remote ? 1 : 0, wait_limit_ns()};
         L.grid = c->grid_cap;
     }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -278,7 +288,7 @@ void do_iterate(jacobi3d* c, int64_t n) {
             c->persist_base += (uint32_t)m;
             if (c->n_remote_done > 0 && !c->skip_exchange) {  // peers' writes into this GPU have landed
                 CK(launch_wait_counters(c->d_remote_done, c->n_remote_done, c->persist_base * c->slab_target,
-                                        c->main));
+                                        wait_limit_ns(), c->main));
                 count_launch(c, -1);
             }
             c->iter += m;
