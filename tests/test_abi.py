@@ -107,3 +107,23 @@ def test_persistent_launch_validation():
     cfg.launch = 3
     assert jb.lib.jacobi3d_plan(ctypes.byref(cfg), ctypes.byref(jb.PlanInfo())) == jb.EINVAL
     del j3d
+
+
+def test_binding_constants_match_header():
+    """Every J3D_* constant the ctypes binding mirrors has the header's value."""
+    import paper_2202_11819_b200.jacobi3d as b
+
+    hdr = {}
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        for name, val in re.findall(r"^#define\s+J3D_(\w+)\s+(-?\d+)\b", open(h).read(), flags=re.M):
+            hdr[name] = int(val)
+    pairs = {"OK": b.OK, "EINVAL": b.EINVAL, "EDECOMP": b.EDECOMP, "ENOMEM": b.ENOMEM, "ECUDA": b.ECUDA,
+             "ENCCL": b.ENCCL, "ENOTLOCAL": b.ENOTLOCAL, "ESTATE": b.ESTATE, "ETIMEOUT": b.ETIMEOUT,
+             "EUNSUPPORTED": b.EUNSUPPORTED, "UNFUSED": b.UNFUSED, "FUSE_A": b.FUSE_A, "FUSE_B": b.FUSE_B,
+             "FUSE_C": b.FUSE_C, "FUSE_DIRECT": b.FUSE_DIRECT, "PER_BLOCK": b.PER_BLOCK, "BATCHED": b.BATCHED,
+             "PERSISTENT": b.PERSISTENT, "XCHG_AUTO": b.XCHG_AUTO, "XCHG_NCCL": b.XCHG_NCCL,
+             "XCHG_P2P": b.XCHG_P2P, "XCHG_HOST": b.XCHG_HOST, "INIT_DEFAULT": b.INIT_DEFAULT,
+             "INIT_CONST": b.INIT_CONST, "INIT_LINEAR": b.INIT_LINEAR, "INIT_HASH": b.INIT_HASH}
+    for k, v in pairs.items():
+        assert hdr.get(k) == v, (k, hdr.get(k), v)
+    assert ctypes.sizeof(b.Config) == 8 * 6 + 4 * 10 + 8  # jacobi3d_config: 6 int64, 10 int32, 1 double
