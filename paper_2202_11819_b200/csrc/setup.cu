@@ -400,11 +400,15 @@ void build_static_tables(jacobi3d* c) {
     // small problems: shorter chunks until there are >= 6 items per CTA slot
     // (at least 24 planes per chunk): the last round of items is then short
     // (measured: 96^3 blocks, ODF 64: 198 -> 225 GLUPS)
-    while (tiles * best_zc < 6 * (int64_t)c->grid_cap && c->nz / (best_zc + 1) >= 24) ++best_zc;
-    // persistent launch with fewer than two items per CTA slot: iterations overlap, so
-    // more, shorter items keep the SMs busy (192^3 on one GPU: 284 -> 342 GLUPS at 16 planes)
-    if (c->cfg.launch == J3D_PERSISTENT)
+    if (c->cfg.launch == J3D_PERSISTENT) {
+        // persistent launch: iterations overlap, so there is no per-iteration tail to
+        // shorten -- two items per CTA slot keep the SMs busy, and longer chunks re-read
+        // fewer boundary planes (96^3 blocks: 24 -> 48 planes, 311 -> 330 GLUPS; 192^3
+        // single block: 16 planes, 284 -> 342 GLUPS)
         while (tiles * best_zc < 2 * (int64_t)c->grid_cap && c->nz / (best_zc + 1) >= 16) ++best_zc;
+    } else {
+        while (tiles * best_zc < 6 * (int64_t)c->grid_cap && c->nz / (best_zc + 1) >= 24) ++best_zc;
+    }
     if (const char* e = std::getenv("J3D_ZCHUNK")) {  // tuning override: planes per z chunk
         const int64_t L = std::atoll(e);
         if (L > 0) best_zc = std::max<int64_t>(1, (c->nz + L - 1) / L);
