@@ -10,7 +10,10 @@ the stencil update of every block plus the pack/exchange/unpack of every face
 hash-random fp64 data (seed 20220223, Dirichlet boundary 1.0).
 
 Default workload (BASELINE.json configs[1], the one the metric is quoted on):
-weak scaling, 1536^3 cells per GPU, ODF=1.  Rank 0 prints ONE JSON line.
+weak scaling, 1536^3 cells per GPU, ODF=1, batched launch (one stencil launch
+per iteration).  The small and fine-grained workloads default to the persistent
+launch (one stencil launch per timed region, --launch overrides).  Rank 0
+prints ONE JSON line.
 """
 from __future__ import annotations
 
