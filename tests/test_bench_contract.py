@@ -44,3 +44,29 @@ def test_workload_launch_defaults_in_config():
     assert cfg("--workload", "small192_odf1", "--grid", "64,64,32")["launch"] == "persistent"
     assert cfg("--workload", "small192_odf1", "--grid", "64,64,32", "--variant", "unfused")["launch"] == "batched"
     assert cfg("--workload", "small192_odf1", "--grid", "64,64,32", "--launch", "per_block")["launch"] == "per_block"
+
+
+def test_weak_scaling_grids_plan_to_fixed_per_gpu_work():
+    """Weak scaling as the driver runs it (N = 1, 2, 4, 8, one rank per GPU):
+    for every weak workload bench.py's global grid plans to the GPU grid
+    weak_global assumes, each GPU owns exactly the per-GPU block split into ODF
+    blocks, peer faces per GPU are 0/1/2/3 and the plan fits one
+    B200's 180 GB of HBM."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import paper_2202_11819_b200 as j3d
+
+    want_grid = {1: (1, 1, 1), 2: (1, 1, 2), 4: (1, 2, 2), 8: (2, 2, 2)}
+    for name, wl in bench.WORKLOADS.items():
+        if wl["kind"] != "weak":
+            continue
+        for n, faces in ((1, 0), (2, 1), (4, 2), (8, 3)):
+            g = bench.weak_global(wl["per_gpu"], n)
+            info = j3d.plan(g, odf=wl["odf"], n_gpus=n, launch=wl.get("launch", "batched"))
+            assert info["gpu_grid"] == want_grid[n], (name, n, info)
+            per_gpu = tuple(b * k for b, k in zip(info["blk_ext"], info["blk_grid"]))
+            assert per_gpu == tuple(wl["per_gpu"]), (name, n, info)
+            assert info["n_blocks"] == wl["odf"] * n
+            if wl["odf"] == 1:
+                assert info["peer_faces_max"] == faces, (name, n, info)
+            assert 0 < info["bytes_per_gpu"] < 180e9, (name, n, info["bytes_per_gpu"])
