@@ -35,3 +35,16 @@ def uniform_field(gx: int, gy: int, gz: int, seed: int, boundary: float = 1.0,
     rng = np.random.default_rng(seed)
     a[1:-1, 1:-1, 1:-1] = rng.uniform(lo, hi, size=(gz, gy, gx))
     return a
+
+
+def sprinkle_nonfinite(a: np.ndarray, seed: int, count: int = 12) -> np.ndarray:
+    """Copy of a ghosted field with ``count`` random owned cells set to +inf,
+    -inf or NaN in turn (non-finite parity cases; R18)."""
+    b = a.copy()
+    gz, gy, gx = (s - 2 for s in a.shape)
+    rng = np.random.default_rng(seed)
+    vals = (math.inf, -math.inf, math.nan)
+    for t in range(count):
+        k, j, i = (int(rng.integers(0, n)) for n in (gz, gy, gx))
+        b[k + 1, j + 1, i + 1] = vals[t % 3]
+    return b

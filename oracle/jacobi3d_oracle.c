@@ -179,15 +179,19 @@ uint64_t oracle_checksum(int64_t gx, int64_t gy, int64_t gz, const double *U) {
 }
 
 /* Residual (R11): max over owned cells of |U - Uprev| (L-infinity
- * norm of the last iteration's change).  Exact, order independent. */
+ * norm of the last iteration's change).  Exact, order independent.  A NaN
+ * change (a NaN cell, or inf - inf) makes the norm NaN: a comparison-based
+ * max would silently skip it (R11, NaN policy). */
 double oracle_residual(int64_t gx, int64_t gy, int64_t gz, const double *U, const double *Uprev) {
     double m = 0.0;
-#pragma omp parallel for schedule(static) reduction(max : m)
+    int any_nan = 0;
+#pragma omp parallel for schedule(static) reduction(max : m) reduction(| : any_nan)
     for (int64_t k = 0; k < gz; ++k)
         for (int64_t j = 0; j < gy; ++j)
             for (int64_t i = 0; i < gx; ++i) {
                 double d = fabs(AT(U, i, j, k) - AT(Uprev, i, j, k));
-                if (d > m) m = d;
+                if (d != d) any_nan = 1;
+                else if (d > m) m = d;
             }
-    return m;
+    return any_nan ? (double)NAN : m;
 }

@@ -30,6 +30,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <type_traits>
 
@@ -163,17 +164,28 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 // the result is q.  Subnormal results and zeros (|s| < 7*2^-1022): s is an
 // integer N times 2^-1074 with |N| < 2^55, and RN(s/7) = 2^-1074 * (N/7
 // rounded to nearest -- 7 is odd, so there are no ties), done in integer
-// arithmetic, with the sign of s (so -0/7 = -0).  DESIGN.md "Division"; checked against __ddiv_rn on the GPU by
-// jacobi3d_div7_selftest.
+// arithmetic, with the sign of s (so -0/7 = -0).  Non-finite s: the fast
+// path gives NaN for s = +-inf (e = inf - inf), so the exact routine returns
+// s * y there (+-inf / 7 = +-inf; NaN stays NaN).  DESIGN.md "Division";
+// checked against __ddiv_rn on the GPU by jacobi3d_div7_selftest.
 constexpr double kDiv7Tiny = 0x1.cp-1020;  // 7 * 2^-1022: below it s/7 is subnormal (or s is 0)
+constexpr double kDiv7Min = 0x1p-1022;     // smallest normal double
 
-// Fast path, valid for |s| >= kDiv7Tiny: three fp64 ops, no branch.
+// Fast path, valid for finite |s| >= kDiv7Tiny: three fp64 ops, no branch.
 __device__ __forceinline__ double div7_fast(double s) {
     const double y = 0x1.2492492492492p-3;  // RN(1/7)
     const double q = __dmul_rn(s, y);
     const double e = __fma_rn(-q, 7.0, s);
     return __fma_rn(e, y, q);  // exact quotients: e == 0 and the result is q
 }
+
+// The stencil's decision: a fast-path result r = div7_fast(s) is kept unless
+// it is zero, subnormal or NaN (one DSETP: !(|r| >= 2^-1022), unordered
+// compare).  Every s outside that set is finite with |s| >= kDiv7Tiny, where
+// the fast path is exact; the set contains every s the fast path can get
+// wrong (+-0 -- it returns +0 for -0 --, the subnormal quotients, +-inf and
+// NaN).  Flagged planes go through div7() below.
+__device__ __forceinline__ bool div7_rare(double r) { return !(fabs(r) >= kDiv7Min); }
 
 // All s (the stencil calls it only on the rare path, see stencil_tma_kernel).
 __device__ __forceinline__ double div7(double s) {
@@ -184,6 +196,8 @@ __device__ __forceinline__ double div7(double s) {
         long long k = a / 7;
         if (a - 7 * k >= 4) k += 1;
         r = copysign(__dmul_rn((double)k, 0x1p-1074), s);  // sign kept for zero results too
+    } else if (!(fabs(s) <= 0x1.fffffffffffffp+1023)) {  // +-inf (an overflowed sum) or NaN
+        r = __dmul_rn(s, 0x1.2492492492492p-3);          // +-inf * y = +-inf; NaN -> NaN
     }
     return r;
 }
@@ -508,8 +522,9 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
         // the owning lane afterwards); 2: any faces, stored inline (fused
         // epilogue, "pack fused into the update").  WHOLE: every cell of the
         // tile is inside the block (no store predicates).  The hot loop has no
-        // branch; a sum whose quotient would be subnormal flags the plane for
-        // a rare exact pass (recompute from the same inputs, store again).
+        // branch; a quotient that is zero, subnormal or NaN (div7_rare: zero,
+        // tiny or non-finite sums) flags the plane for a rare exact pass
+        // (recompute from the same inputs, store again).
         auto compute_plane = [&](auto mode_tag, auto whole_tag, int z, uint32_t fm, const double* pm,
                                  const double* pc, const double* pp) {
             constexpr int MODE = decltype(mode_tag)::value;
@@ -555,7 +570,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                     ypd = F.p + (int64_t)z * F.sb;
                 }
             }
-            bool tiny = false;
+            bool rare = false;
 #pragma unroll
             for (int r = 0; r < RPW; ++r) {
 #pragma unroll
@@ -569,8 +584,8 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                     const double2 zp = *reinterpret_cast<const double2*>(pp + off);
                     const double s0 = sum7(cc.x, p[-1], cc.y, ym.x, yp.x, zm.x, zp.x);
                     const double s1 = sum7(cc.y, cc.x, p[2], ym.y, yp.y, zm.y, zp.y);
-                    tiny |= (fabs(s0) < kDiv7Tiny) | (fabs(s1) < kDiv7Tiny);
                     const double vx = div7_fast(s0), vy = div7_fast(s1);
+                    rare |= div7_rare(vx) | div7_rare(vy);
                     if constexpr (MODE == 1) {
                         if (c == 0) cap0[r] = vx;
                         if (c == clast) cap1[r] = last_is_x ? vx : vy;
@@ -635,7 +650,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                         }
                 }
             }
-            if (tiny || rare_faces) {
+            if (rare || rare_faces) {
 #pragma unroll
                 for (int r = 0; r < RPW; ++r) {
 #pragma unroll
@@ -644,7 +659,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                         if (y >= ny || x >= nx) continue;
                         const bool has2 = x + 1 < nx;
                         const bool onb = (rare_faces & 48u) != 0;
-                        if (!tiny && !onb) continue;
+                        if (!rare && !onb) continue;
                         const int off = r * W + 64 * c;
                         const double* p = pc + off;
                         const double2 cc = *reinterpret_cast<const double2*>(p);
@@ -657,8 +672,8 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                         double* o = op + r * pitch + 64 * c;
                         o[0] = vx;
                         if (has2) o[1] = vy;
-                        // tiny sums: redo every face store of this cell with the exact value
-                        const uint32_t m = tiny ? fm : (rare_faces & fm);
+                        // rare quotients: redo every face store of this cell with the exact value
+                        const uint32_t m = rare ? fm : (rare_faces & fm);
                         if (m) epi_store(d, m, x, y, z, vx, vy, has2);
                     }
                 }
@@ -697,7 +712,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                     ypd = F.p + (int64_t)z * F.sb;
                 }
             }
-            bool tiny = false;
+            bool rare = false;
 #pragma unroll
             for (int r = 0; r < RPW; ++r) {
 #pragma unroll
@@ -709,8 +724,8 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                     const int om = (k == 0 && xlf) ? xlb + r * (1 - W) : -1;
                     const int oq = (k == kedge && xrf) ? xrb + r * (1 - W) : 1;
                     const double sv = sum7(p[0], p[om], p[oq], p[-W], p[W], pm[off], pp[off]);
-                    tiny |= fabs(sv) < kDiv7Tiny;
                     const double v = div7_fast(sv);
+                    rare |= div7_rare(v);
                     if constexpr (MODE >= 1) {
                         if (k == 0) cap0[r] = v;
                         if (k == klast) cap1[r] = v;
@@ -749,7 +764,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                         }
                 }
             }
-            if (tiny || rare_faces) {
+            if (rare || rare_faces) {
 #pragma unroll
                 for (int r = 0; r < RPW; ++r) {
 #pragma unroll
@@ -762,7 +777,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                         const int oq = (k == kedge && xrf) ? xrb + r * (1 - W) : 1;
                         const double v = div7(sum7(p[0], p[om], p[oq], p[-W], p[W], pm[off], pp[off]));
                         op[r * pitch + 32 * k] = v;
-                        const uint32_t m = tiny ? fm : (rare_faces & fm);
+                        const uint32_t m = rare ? fm : (rare_faces & fm);
                         // epi_store writes pairs; pass (v, v) with has2 = false
                         if (m) epi_store(d, m, x, y, z, v, v, false);
                     }
@@ -914,43 +929,74 @@ __global__ void __launch_bounds__(256) residual_kernel(const BlockGeom* __restri
     const double* u = b.buf[which];
     const double* v = b.buf[which ^ 1];
     const int64_t n = (int64_t)b.nx * b.ny * b.nz;
-    double m = 0.0;
+    // max over the bit patterns of |u - v|: non-negative doubles order like
+    // their bit patterns, and a NaN difference (bits above +inf's) wins, so a
+    // NaN anywhere makes the residual NaN (R11; fmax would drop it)
+    unsigned long long m = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t x = i % b.nx, t = i / b.nx, y = t % b.ny, z = t / b.ny;
         const int64_t o = (z + 1) * b.zs + (y + 1) * b.pitch + XOFF + x;
-        m = fmax(m, fabs(u[o] - v[o]));
+        const unsigned long long d = (unsigned long long)__double_as_longlong(fabs(__dsub_rn(u[o], v[o])));
+        m = d > m ? d : m;
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    // non-negative doubles order like their bit patterns
-    if ((threadIdx.x & 31) == 0) atomicMax(acc, (unsigned long long)__double_as_longlong(m));
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, m, o);
+        m = t > m ? t : m;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(acc, m);
 }
 
 // ------------------------------------------------------------------ division self-test
-// Compares div7 with the IEEE division routine on n inputs drawn from
-// splitmix64: mode 0 = random bit patterns (all finite doubles, including
-// subnormals), 1 = uniform in [0,7) (the workloads' range), 2 = small
-// integers times 2^-k (exact / tie-prone quotients), 3 = |s| near the
-// subnormal boundary.
+// Compares the stencil's division -- r = div7_fast(s), replaced by div7(s)
+// when div7_rare(r) -- and div7 alone with the IEEE division routine on n
+// inputs drawn from splitmix64: mode 0 = random bit patterns (every double:
+// subnormals, +-inf and NaNs included), 1 = uniform in [0,7) (the workloads'
+// range), 2 = small integers times 2^-k (exact / tie-prone quotients), 3 =
+// |s| near the subnormal boundary, 4 = the special values +-0, +-inf, NaN,
+// +-DBL_MAX and its neighbours, +-min normal, +-min subnormal, 5 = |s| in
+// the top binades (sums near overflow), 6 = |s| within 2^-10 of
+// 7*2^-1022 (the fast path's stated lower limit).  NaN results compare by
+// NaN-ness only (NaN payloads are not part of the result).
+__device__ __forceinline__ bool div7_same(double a, double b) {
+    if (isnan(b)) return isnan(a);
+    return __double_as_longlong(a) == __double_as_longlong(b);
+}
+
 __global__ void div7_selftest_kernel(uint64_t n, uint64_t seed, unsigned long long* bad, double* example) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t h = splitmix64(seed ^ (i * 0x9E3779B97F4A7C15ULL));
-        const int mode = (int)(i & 3);
+        const int mode = (int)(i % 7);
         double s;
         if (mode == 0) {
             s = __longlong_as_double((long long)h);
-            if (isnan(s) || isinf(s)) continue;
         } else if (mode == 1) {
             s = (double)(h >> 11) * 0x1p-53 * 7.0;
         } else if (mode == 2) {
             s = ldexp((double)((long long)(h >> 40) - (1LL << 23)), -(int)((h >> 8) & 63));
-        } else {
+        } else if (mode == 3) {
             s = ldexp((double)(h >> 11) * 0x1p-53 + 0.5, -1016 - (int)((h >> 4) & 63));
             if (h & 1) s = -s;
+        } else if (mode == 4) {
+            const uint64_t special[10] = {0x0ULL, 0x7ff0000000000000ULL, 0x7ff8000000000000ULL, 0x7fefffffffffffffULL,
+                                          0x0010000000000000ULL, 0x1ULL, 0x7feffffffffffff0ULL, 0x7ff4000000000001ULL,
+                                          0x000fffffffffffffULL, 0x001c000000000000ULL};
+            uint64_t b = special[(h >> 1) % 10];
+            if ((h >> 8) & 1) b = (b - ((h >> 16) & 15)) & 0x7fffffffffffffffULL;  // neighbours below
+            s =__longlong_as_double((long long)(b | ((h & 1) << 63)));  // both signs
+        } else if (mode == 5) {
+            s = ldexp((double)(h >> 11) * 0x1p-53 + 0.5, 1024 - (int)((h >> 4) & 7));
+            if (h & 1) s = -s;
+        } else {
+            s = __dmul_rn(0x1.cp-1020, 1.0 + ldexp((double)((long long)(h >> 32) - (1LL << 31)), -41));
+            if (h & 1) s = -s;
         }
-        const double a = div7(s), b = __ddiv_rn(s, 7.0);
-        if (__double_as_longlong(a) != __double_as_longlong(b)) {
-            if (atomicAdd(bad, 1ULL) == 0) { example[0] = s; example[1] = a; example[2] = b; }
+        const double b = __ddiv_rn(s, 7.0);
+        double a = div7_fast(s);
+        if (div7_rare(a)) a = div7(s);
+        const double c = div7(s);
+        if (!div7_same(a, b) || !div7_same(c, b)) {
+            if (atomicAdd(bad, 1ULL) == 0) { example[0] = s; example[1] = div7_same(a, b) ? c : a; example[2] = b; }
         }
     }
 }
@@ -990,12 +1036,17 @@ cudaError_t launch_div7_selftest(uint64_t n, uint64_t seed, unsigned long long* 
 
 template <class T>
 static cudaError_t launch_t(const StencilLaunch& L, cudaStream_t st) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(stencil_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             T::SMEM_BYTES);
+    // once per device (the attribute belongs to the device's context); ranks may
+    // be threads of one process, on one device or several
+    static std::atomic<uint64_t> attr_set{0};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(attr_set.load(std::memory_order_acquire) & bit)) {
+        e = cudaFuncSetAttribute(stencil_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM_BYTES);
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_set.fetch_or(bit, std::memory_order_acq_rel);
     }
     if (L.n_items <= 0) return cudaSuccess;
     stencil_tma_kernel<T><<<L.grid, T::THREADS, T::SMEM_BYTES, st>>>(

@@ -11,7 +11,7 @@ import itertools
 import numpy as np
 import pytest
 
-from inputs.generators import sine_mode, uniform_field
+from inputs.generators import sine_mode, sprinkle_nonfinite, uniform_field
 from oracle import core
 from tests.helpers import assert_bitwise, gpu_run, oracle_initial
 
@@ -170,10 +170,13 @@ def test_get_region_matches_get_block():
 
 
 def test_div7_matches_ieee_division():
-    """The stencil's s/7 (Markstein-corrected reciprocal + exact integer path
-    for subnormal quotients) is bitwise the IEEE
-    round-to-nearest division on 2^27 inputs per seed, including random bit
-    patterns, subnormals and exact/tie-prone dyadic values."""
+    """The stencil's s/7 (Markstein-corrected reciprocal, kept unless the
+    quotient is zero, subnormal or NaN; then the exact routine: integer path
+    for subnormal quotients, s*y for +-inf) is the IEEE
+    round-to-nearest division on 2^27 inputs per seed: random bit patterns
+    (every double, +-inf and NaNs included), subnormals, exact/tie-prone
+    dyadic values, +-0, +-DBL_MAX and the top binades (sums near overflow).
+    NaN results compare by NaN-ness (R18)."""
     from paper_2202_11819_b200.jacobi3d import div7_selftest
 
     for seed in (1, 2):
@@ -240,3 +243,48 @@ def test_plan_bytes_match_allocation(grid, odf, launch):
     with j3d.Jacobi3D(grid, odf=odf, variant="direct", launch=launch) as ctx:
         rec = ctx.ipc_export()
     assert struct.unpack_from("<Q", rec, 16)[0] == want
+
+
+def _same_or_both_nan(got, want):
+    got = np.asarray(got, dtype=np.float64)
+    want = np.ascontiguousarray(want, dtype=np.float64)
+    ng, nw = np.isnan(got), np.isnan(want)
+    if not (ng == nw).all():
+        bad = np.argwhere(ng != nw)
+        raise AssertionError(f"NaN-ness differs in {len(bad)} cells, first {bad[0].tolist()}")
+    assert_bitwise(np.where(ng, 0.0, got), np.where(nw, 0.0, want), "non-NaN cells")
+
+
+def _case_nonfinite(grid, odf, variant, launch, n, kind="default", params=None, boundary=1.0, field=None):
+    """NaN policy (R18): NaN-ness equal and every other cell bit for
+    bit; the checksum (bits of every cell) only where no cell is NaN; the
+    residual NaN-ness or bits."""
+    with j3d.Jacobi3D(grid, odf=odf, variant=variant, launch=launch, boundary=boundary) as ctx:
+        got = gpu_run(ctx, n, kind, params, 0, field)
+        ck = ctx.checksum()
+        res = ctx.residual()
+    U0 = field if field is not None else oracle_initial(grid, kind, params or (0, 0, 0, 0), 0, boundary)
+    want, prev = core.run_pair(U0, n)
+    W = core.owned(want)
+    _same_or_both_nan(got, W)
+    if not np.isnan(W).any():
+        assert ck == core.checksum(want)
+    r = core.residual(want, prev)
+    assert (np.isnan(res) and np.isnan(r)) or np.float64(res).tobytes() == np.float64(r).tobytes(), (res, r)
+
+
+@pytest.mark.parametrize("variant,launch", [("direct", "batched"), ("direct", "persistent"), ("C", "batched"),
+                                            ("unfused", "per_block")])
+def test_nonfinite_values(variant, launch):
+    """IEEE semantics of S:388's sum and /7 for non-finite values (the oracle's
+    pins: test_oracle_pins non-finite section): a +-inf Dirichlet boundary,
+    a constant field whose sum overflows (1e308, -DBL_MAX), and a field with
+    +-inf / NaN cells (inf - inf = NaN spreads) -- the stencil's rare path
+    must give +-inf where the fast division would give NaN."""
+    grid = (70, 34, 20)
+    _case_nonfinite(grid, 4, variant, launch, 6, boundary=float("inf"))
+    _case_nonfinite(grid, 4, variant, launch, 6, boundary=float("-inf"))
+    _case_nonfinite(grid, 4, variant, launch, 3, kind="const", params=(1e308,))
+    _case_nonfinite(grid, 4, variant, launch, 3, kind="const", params=(-float.fromhex("0x1.fffffffffffffp+1023"),))
+    U0 = sprinkle_nonfinite(uniform_field(*grid, seed=13, boundary=0.5), seed=5)
+    _case_nonfinite(grid, 4, variant, launch, 5, boundary=0.5, field=U0)

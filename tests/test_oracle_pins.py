@@ -320,3 +320,93 @@ def test_residual_pins():
     a, b = core.run_pair(core.init(4, 4, 4), 2)
     assert abs(core.residual(a, b) - 9 / 49) <= 4 * EPS
     assert core.residual(a, b) == twin.residual(a, b)
+
+
+# ---------------------------------------------------------------- non-finite values (IEEE 754 semantics)
+
+def _same_or_both_nan(a: np.ndarray, b: np.ndarray) -> bool:
+    """NaN policy (R18): NaN-ness must agree, payloads are not part of
+    the result; every other value bit for bit."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    na, nb = np.isnan(a), np.isnan(b)
+    return bool((na == nb).all() and (a[~na].view(np.uint64) == b[~nb].view(np.uint64)).all())
+
+
+@pytest.mark.parametrize("inf", [math.inf, -math.inf])
+def test_infinite_boundary_one_iteration(inf):
+    """IEEE 754 (S:388's sum and /7 carried out in binary64): x + inf = inf for
+    finite x and inf / 7 = inf.  4^3 grid, interior 0, Dirichlet boundary
+    +-inf: after one iteration each of the 56 cells next to the boundary is
+    +-inf and the inner 2x2x2 stays 0; the ghost shell is unchanged."""
+    U = core.run(core.init(4, 4, 4, boundary=inf), 1)
+    O = core.owned(U)
+    for k in range(4):
+        for j in range(4):
+            for i in range(4):
+                want = inf if _class_of(i, j, k) > 0 else 0.0
+                assert O[k, j, i] == want, (i, j, k, O[k, j, i])
+    assert (U[0] == inf).all() and (U[:, 0] == inf).all()
+    # two more iterations: the scalar IEEE brute force agrees bit for bit
+    B = brute.run_float(brute.make_grid(4, 4, 4, 0.0, inf), 4, 4, 4, 3)
+    assert _same_or_both_nan(core.run(core.init(4, 4, 4, boundary=inf), 3), np.array(B))
+
+
+@pytest.mark.parametrize("c", [1e308, -1e308, float.fromhex("0x1.fffffffffffffp+1023")])
+def test_overflowing_sum_is_infinite(c):
+    """IEEE 754 round-to-nearest overflow: a constant field c with |7c| > DBL_MAX
+    (2c already overflows) sums to +-inf in S:388's order, and +-inf / 7 = +-inf:
+    every owned cell is +-inf after one iteration (the CONST init fills the
+    ghost shell with c as well)."""
+    U = core.run(core.init(5, 4, 3, core.INIT_CONST, (c,)), 1)
+    assert (core.owned(U) == math.copysign(math.inf, c)).all()
+    assert (U[0] == c).all()
+
+
+def test_mixed_infinities_give_nan_like_brute_force():
+    """+inf boundary and one -inf interior cell: cells that see both get
+    inf + (-inf) = NaN (IEEE 754 invalid operation), which then spreads.  The C
+    oracle and the scalar brute force agree cell by cell (NaN-ness; R18)."""
+    G = brute.make_grid(4, 4, 4, 0.0, math.inf)
+    G[2][2][2] = -math.inf
+    U = core.init(4, 4, 4, boundary=math.inf)
+    U[2, 2, 2] = -math.inf
+    for n in (1, 2, 3):
+        want = np.array(brute.run_float([[row[:] for row in p] for p in G], 4, 4, 4, n))
+        got = core.run(U, n)
+        assert np.isnan(got).any() and _same_or_both_nan(got, want), n
+        assert _same_or_both_nan(got, twin.run(U, n)), n
+
+
+def test_residual_nan_policy():
+    """Residual (R11) of a field whose change is NaN somewhere (inf - inf after
+    the overflowed constant field, or a NaN cell) is NaN -- the numpy twin's
+    np.max propagates NaN the same way -- and +inf for a finite -> inf change."""
+    a, b = core.run_pair(core.init(3, 3, 3, core.INIT_CONST, (1e308,)), 2)  # inf - inf
+    assert math.isnan(core.residual(a, b)) and math.isnan(twin.residual(a, b))
+    a, b = core.run_pair(core.init(3, 3, 3, core.INIT_CONST, (1e308,)), 1)  # inf - 1e308
+    assert core.residual(a, b) == math.inf == twin.residual(a, b)
+    U = core.init(6, 5, 4, core.INIT_HASH, seed=3)
+    V = U.copy()
+    V[2, 3, 4] = math.nan
+    assert math.isnan(core.residual(U, V)) and math.isnan(core.residual(V, U))
+    assert math.isnan(twin.residual(U, V))
+
+
+# ---------------------------------------------------------------- the timing sweep
+
+@pytest.mark.parametrize("grid,kind,seed", [((9, 7, 5), core.INIT_HASH, 1), ((16, 12, 10), core.INIT_HASH, 2),
+                                            ((8, 8, 8), core.INIT_DEFAULT, 0)])
+def test_sweep_owned_equals_sweep(grid, kind, seed):
+    """oracle_sweep_owned (the cpu_baseline / reference-arm sweep) skips the
+    ghost-shell copy; with both buffers carrying the same Dirichlet shell it
+    must give oracle_sweep's owned cells bit for bit, iteration after
+    iteration, and leave the shell untouched."""
+    U = core.init(*grid, kind, seed=seed)
+    A, B = U.copy(), U.copy()
+    ref = U
+    for _ in range(4):
+        core.sweep_owned_timing(A, B)
+        A, B = B, A
+        ref = core.sweep(ref)
+        assert A.tobytes() == ref.tobytes()
