@@ -123,21 +123,43 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def traffic_from_profiles(workload):
-    """dram__bytes_read.sum + dram__bytes_write.sum per stencil launch from the
-    committed ncu --set full summary (profiles/ncu_stencil_*.json), if any."""
+def lib_sha256():
+    """sha256 of the loaded libjacobi3d.so: ties an ncu capture to the build."""
+    import hashlib
+
+    from paper_2202_11819_b200 import jacobi3d as jb
+
+    with open(jb.LIB_PATH, "rb") as f:
+        return hashlib.sha256(f.read()).hexdigest()
+
+
+def traffic_from_profiles(workload, launch, variant, tile_kind, steps):
+    """dram__bytes_read.sum + dram__bytes_write.sum per stencil launch from a
+    committed ncu --set full summary (profiles/ncu_stencil_*.json) -- only one
+    captured from THIS build (sha256 of the library) with the same workload,
+    launch mode, variant and tile kind (and, for the persistent launch, the
+    same iterations per launch); otherwise None and the reason."""
     import glob
 
-    best = None
+    sha = lib_sha256()
+    why = "no committed ncu capture for this workload"
     for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_stencil_*.json"))):
         try:
             with open(p) as f:
                 d = json.load(f)
         except Exception:
             continue
-        if d.get("workload") == workload and d.get("traffic_bytes_per_launch"):
-            best = d
-    return best
+        if d.get("workload") != workload or not d.get("traffic_bytes_per_launch"):
+            continue
+        want = {"lib_sha256": sha, "launch": launch, "variant": variant, "tile_kind": tile_kind}
+        if launch == "persistent":
+            want["iters_per_launch"] = steps
+        bad = [k for k, v in want.items() if d.get(k) != v]
+        if bad:
+            why = f"{os.path.basename(p)}: {', '.join(bad)} differ from this run"
+            continue
+        return d, os.path.basename(p)
+    return None, why
 
 
 def cpu_baseline(workload_grid, budget_s=12.0):
@@ -161,6 +183,7 @@ def cpu_baseline(workload_grid, budget_s=12.0):
         if el > budget_s or n >= 1000:
             break
     lups = gx * gy * slab * n
+    el_all = el
     # the same sweep on one core (the oracle at all cores and at 1 core)
     cores = core.threads()
     core.set_threads(1)
@@ -176,10 +199,25 @@ def cpu_baseline(workload_grid, budget_s=12.0):
     finally:
         core.set_threads(cores)
     del U, V
-    return {"value": lups / el / 1e9, "unit": "GLUPS", "cores": cores, "kind": "oracle",
-            "value_1core": gx * gy * slab * n1 / el1 / 1e9,
+    return {"value": lups / el_all / 1e9, "unit": "GLUPS", "cores": cores, "kind": "oracle",
+            "value_1core": gx * gy * slab * n1 / el1 / 1e9, **host_cpu(),
             "sample": f"{n} full sweeps of a {gx}x{gy}x{slab} slab of the workload (hash init, seed {SEED}), "
-                      f"{el:.1f} s on {cores} threads; {n1} sweeps in {el1:.1f} s on 1 thread"}
+                      f"{el_all:.1f} s on {cores} threads; {n1} sweeps in {el1:.1f} s on 1 thread"}
+
+
+def host_cpu():
+    """The host the oracle ran on (nproc and the CPU model)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    aff = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else None
+    return {"cpu_model": model, "nproc": aff or os.cpu_count(), "cpu_count": os.cpu_count()}
 
 
 def parse():
@@ -200,6 +238,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--grid", default=None, help="override global grid gx,gy,gz")
     ap.add_argument("--odf", type=int, default=None)
+    ap.add_argument("--repeats", type=int, default=3,
+                    help="timed regions of exactly K steps each; value = their mean (PAPER.md L583-584: "
+                         "averages of 3 runs)")
     return ap.parse_args()
 
 
@@ -259,18 +300,29 @@ def main():
     clk = ClockSampler(local)
     clk.start()
     time.sleep(0.3)
-    ms = ctx.time(0, a.steps)  # CUDA events on the library's stream around exactly K steps
+    reps = []
+    for _ in range(max(1, a.repeats)):
+        # CUDA events on the library's stream around exactly K steps (jacobi3d_time:
+        # stream sync + barrier over ranks before the start event)
+        ms_r = ctx.time(0, a.steps)
+        t = torch.tensor([ms_r], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max over ranks
+        reps.append(float(t.item()))
     clocks = clk.stop()
     prof_ms, prof_n, prof_bytes = ctx.profile_read()
     ctx.profile_enable(False)
-    launches = ctx.stats()["kernel_launches"]
+    st = ctx.stats()
+    launches = st["kernel_launches"] // len(reps)  # per timed region of K steps
     torch.cuda.synchronize()
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
-    ms = float(t.item())
+    ms = statistics.mean(reps)
     value = lups_step * a.steps / (ms * a.steps * 1e-3) / 1e9
+    repeats = {"n": len(reps), "ms_per_step": [round(x, 4) for x in reps], "mean_ms": round(ms, 4),
+               "min_ms": round(min(reps), 4), "value_mean": round(value, 3),
+               "value_best": round(lups_step / (min(reps) * 1e-3) / 1e9, 3),
+               "what": "value = mean over repeats of the max-over-ranks ms/step of K timed steps"}
 
     peak, peak_src = load_peaks()
     roof = None
@@ -281,10 +333,11 @@ def main():
             # per-block launches run concurrently on their own streams: their
             # event times overlap, so use all stencil bytes over the step time
             achieved = prof_bytes / (ms * a.steps * 1e-3) / 1e9
-        tr = traffic_from_profiles(a.workload)
+        tr, tr_src = traffic_from_profiles(a.workload, a.launch, a.variant, st.get("tile_kind"), a.steps)
         roof = {"bound": "hbm", "kernel": "stencil_tma_kernel", "achieved": round(achieved, 1), "peak": peak,
                 "unit": "GB/s", "frac": round(achieved / peak, 4),
-                "traffic": tr["traffic_bytes_per_launch"] if tr else None,
+                "traffic": tr["traffic_bytes_per_launch"] if tr else None, "traffic_source": tr_src,
+                "tile_kind": st.get("tile_kind"),
                 "alg_bytes_per_launch": prof_bytes / prof_n, "avg_launch_ms": avg_ms,
                 "share_of_step": round(prof_ms / (ms * a.steps), 4), "peak_source": peak_src,
                 "method": ("stencil bytes in the timed region / step time (per-block launches overlap)"
@@ -317,7 +370,8 @@ def main():
                 "data": "synthetic", "config": cfg_json,
                 "hbm_gbs_per_gpu": round(value / n * BYTES_PER_LUP, 1),
                 "hbm_frac_per_gpu": round(value / n * BYTES_PER_LUP / peak, 4),
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks}
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+                "repeats": repeats}
         if halo:
             line["halo"] = halo
         print(json.dumps(line), flush=True)
@@ -409,7 +463,7 @@ def reference_arm(a, grid, cfg_json):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg_json,
             "impl": "reference",
             "cpu_baseline": {"value": round(value, 4), "unit": "GLUPS", "cores": core.threads(), "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, **host_cpu()},
             "e2e": {"value": round(value, 4), "unit": "GLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

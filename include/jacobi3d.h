@@ -19,12 +19,23 @@
  *     never retains them after the call returns.  All device memory, streams,
  *     events, CUDA graphs and the NCCL communicator are owned by the context
  *     and released by jacobi3d_destroy.
- *   - A context is bound to one CUDA device and is not thread safe.
- *   - Multi-GPU (n_gpus > 1): one process per GPU (SPMD, e.g. torchrun).
+ *   - A context is bound to one CUDA device and is not thread safe (one
+ *     thread per context; different contexts may be driven concurrently).
+ *   - Multi-GPU (n_gpus > 1): one rank per GPU -- a process per GPU (SPMD,
+ *     e.g. torchrun) -- or ranks as threads of ONE process, several of which
+ *     may share a GPU (dist.ThreadGroup: how the multi-rank paths run on a
+ *     one-GPU machine).  Ranks that share a GPU must be threads of one
+ *     process (J3D_EUNSUPPORTED otherwise: separate processes are separate
+ *     CUDA contexts, which a GPU time-slices, and cross-rank waits need the
+ *     ranks to run at the same time).
  *     create / ipc_connect / init / refresh_halos / iterate / residual /
- *     checksum / destroy are collective: every rank calls them in the same
- *     order with the same arguments.  get_block / set_block / block_info are
- *     rank-local.
+ *     checksum / time / destroy are collective: every rank calls them in the
+ *     same order with the same arguments.  get_block / set_block / block_info
+ *     are rank-local.
+ *   - Control plane (barrier, residual max, checksum sum): NCCL when the
+ *     exchange backend is J3D_XCHG_NCCL, else one POSIX shared-memory
+ *     segment per rank (same node; control.cu) -- no NCCL communicator is
+ *     created for the P2P and host-staging backends.
  *   - Block data on the host is the block's owned cells, extent[2] planes of
  *     extent[1] rows of extent[0] doubles, x fastest (no ghost shell).
  */
@@ -148,6 +159,8 @@ typedef struct {
     int64_t last_graph_parity;/* parity of the last graph launched (-1 if none)                 */
     int64_t launches_per_iter_block; /* kernel launches per interior block per iteration of the
                                         configured variant (13/8/3/1/1)              */
+    int64_t tile_kind;        /* stencil tile configuration in use (kernels.cu J3D_TILES row)    */
+    int64_t work_items;       /* stencil work items (tile x z chunk) per iteration on this rank  */
 } jacobi3d_stats;
 
 /* Plan the decomposition without touching a GPU (PAPER.md
@@ -156,24 +169,45 @@ typedef struct {
  * used only for local_faces.  Returns J3D_EINVAL / J3D_EDECOMP on bad input. */
 J3D_API int jacobi3d_plan(const jacobi3d_config *cfg, jacobi3d_plan_info *out);
 
+/* Plan-only (no GPU) export of the persistent launch's dependency lists
+ * (J3D_PERSISTENT): the slabs of rank cfg->rank are (block,
+ * z chunk zc, tile row ty) with nzc z chunks per block (chunk zc = planes
+ * [nz*zc/nzc, nz*(zc+1)/nzc)) and tile rows of tile_ty rows; an item of
+ * iteration k of a slab starts once every slab in its list finished
+ * iteration k-1.  Writes one row of 7 int64 per list entry: block id, zc,
+ * ty, then the listed slab's owner rank, block id, zc, ty (peer slabs are
+ * the ones whose counters are read over NVLink).  host_out may be NULL;
+ * at most cap_rows rows are written; *n_rows = the total.  The same code
+ * builds the context's device tables (setup.cu slab_dep_refs). */
+J3D_API int jacobi3d_debug_slab_deps(const jacobi3d_config *cfg, int32_t tile_ty, int32_t nzc, int64_t *host_out,
+                                     int64_t cap_rows, int64_t *n_rows);
+
 /* Fill out[128] with an NCCL unique id (call on rank 0 only, broadcast the
  * bytes to every rank before jacobi3d_create). */
 J3D_API int jacobi3d_nccl_unique_id(uint8_t out[128]);
 
 /* Create a context: plan, allocate every block's two ghosted buffers and face
- * buffers on cfg->device, create streams/events, and (n_gpus > 1) initialise
- * the NCCL communicator from nccl_uid (NULL allowed when n_gpus == 1).
- * With the P2P backend the context must then be connected with
- * jacobi3d_ipc_export / jacobi3d_ipc_connect before init.  On failure
- * everything allocated is freed and *out is NULL. */
+ * buffers on cfg->device, create streams/events, load every kernel it will
+ * launch (no lazy loading while ranks wait on each other), and for n_gpus > 1
+ * take nccl_uid (128 bytes, identical on every rank; NULL allowed when
+ * n_gpus == 1) as the job's key: the NCCL communicator's unique id with the
+ * NCCL backend, else the name of the shared-memory control plane (any 128
+ * bytes unique to the job).  A context with n_gpus > 1 must then be
+ * connected with jacobi3d_ipc_export / jacobi3d_ipc_connect before init.
+ * On failure everything allocated is freed and *out is NULL. */
 J3D_API int jacobi3d_create(const jacobi3d_config *cfg, const uint8_t *nccl_uid, jacobi3d_t **out);
 
-/* P2P bootstrap.  export writes this rank's CUDA IPC handle record into
+/* Multi-rank bootstrap.  export writes this rank's connection record into
  * host_out (capacity cap bytes, *len = bytes written; record size is
- * constant for a context).  The caller all-gathers the records (e.g. with
- * torch.distributed) into rank order and passes the concatenation to
- * connect, which maps the neighbours' device memory.  Both are no-ops
- * returning J3D_OK when no peer face uses P2P. */
+ * constant): the CUDA IPC handle of its arena, the arena's address (for
+ * peers that are threads of the same process, which cannot open their own
+ * IPC handle), a process token and the GPU's UUID.  The caller all-gathers
+ * the records (torch.distributed, or dist.ThreadGroup for thread ranks) into
+ * rank order and passes the concatenation to connect (collective), which
+ * maps the neighbours' device memory (P2P), the neighbours' staging
+ * segments (host backend) and every rank's control segment, and ends with a
+ * barrier.  connect returns J3D_EUNSUPPORTED if ranks of different processes
+ * share a GPU, or a P2P peer's GPU is not reachable.  n_gpus == 1: no-op. */
 J3D_API int jacobi3d_ipc_export(jacobi3d_t *ctx, uint8_t *host_out, size_t cap, size_t *len);
 J3D_API int jacobi3d_ipc_connect(jacobi3d_t *ctx, const uint8_t *host_all, size_t len_per_rank);
 
@@ -228,8 +262,9 @@ J3D_API int jacobi3d_residual(jacobi3d_t *ctx, double *out);
 J3D_API int jacobi3d_checksum(jacobi3d_t *ctx, uint64_t *out);
 
 /* Timed run: warmup iterations, then iters iterations bracketed by CUDA
- * events on the context's main stream (after a device synchronize and, for
- * n_gpus > 1, a barrier).  *ms_per_iter = this rank's elapsed / iters. */
+ * events on the context's main stream (after waiting for the context's
+ * streams and, for n_gpus > 1, a barrier).  *ms_per_iter = this rank's
+ * elapsed / iters.  Collective. */
 J3D_API int jacobi3d_time(jacobi3d_t *ctx, int64_t warmup, int64_t iters, double *ms_per_iter);
 /* (J3D_PERSISTENT: the timed iters iterations are one launch.) */
 
@@ -250,15 +285,18 @@ J3D_API int jacobi3d_profile_read(jacobi3d_t *ctx, double *total_ms, int64_t *la
 J3D_API int jacobi3d_set_skip_exchange(jacobi3d_t *ctx, int skip);
 
 /* Self-test of the stencil's division by 7: on the
- * current CUDA device, compare the kernel's correctly rounded s/7 with the
- * IEEE division routine (__ddiv_rn) for n generated inputs (random finite bit
- * patterns incl. subnormals, [0,7), dyadic integers, near-subnormal sums).
+ * current CUDA device, compare the kernel's correctly rounded s/7 -- the
+ * fast path with the stencil's rare-path decision, and the exact routine --
+ * with the IEEE division routine (__ddiv_rn) for n generated inputs (every
+ * bit pattern incl. subnormals, +-inf and NaN, [0,7), dyadic integers,
+ * near-subnormal and near-overflow sums, +-0, +-DBL_MAX); NaN results
+ * compare by NaN-ness.
  * *mismatches = number of differing results; example[3] (may be NULL) =
  * first failing s, kernel result, IEEE result. */
 J3D_API int jacobi3d_div7_selftest(uint64_t n, uint64_t seed, uint64_t *mismatches, double *example);
 
 /* Free everything.  NULL-safe.  Collective when n_gpus > 1: it begins with a
- * barrier over the context's communicator, so no peer can still read (persistent
+ * barrier over the control plane, so no peer can still read (persistent
  * launch: slab counters) or write (epilogue / pack stores) this rank's memory
  * when it is freed. */
 J3D_API int jacobi3d_destroy(jacobi3d_t *ctx);

@@ -102,6 +102,46 @@ int jacobi3d_plan(const jacobi3d_config* cfg, jacobi3d_plan_info* out) {
     });
 }
 
+int jacobi3d_debug_slab_deps(const jacobi3d_config* cfg, int32_t tile_ty, int32_t nzc, int64_t* host_out,
+                             int64_t cap_rows, int64_t* n_rows) {
+    return guarded([&]() -> int {
+        if (!n_rows) return fail(J3D_EINVAL, "n_rows is NULL");
+        int rc = validate_cfg(cfg);
+        if (rc) return rc;
+        if (tile_ty < 1 || nzc < 1) return fail(J3D_EINVAL, "tile_ty and nzc must be >= 1");
+        jacobi3d c;  // host-side state only: plan and face classification, no device
+        c.cfg = *cfg;
+        c.rank = cfg->rank;
+        c.n_gpus = cfg->n_gpus;
+        std::string msg;
+        rc = make_plan({cfg->gx, cfg->gy, cfg->gz}, {cfg->bx, cfg->by, cfg->bz}, cfg->odf, cfg->n_gpus, c.plan, msg);
+        if (rc) return fail(rc, msg);
+        if (nzc > c.plan.ext[2]) return fail(J3D_EINVAL, "more z chunks than planes");
+        classify(&c);
+        const int nty = (int)((c.plan.ext[1] + tile_ty - 1) / tile_ty);
+        const auto refs = slab_dep_refs(&c, nzc, nty);
+        int64_t rows = 0;
+        for (int l = 0; l < c.n_local; ++l)
+            for (int zc = 0; zc < nzc; ++zc)
+                for (int ty = 0; ty < nty; ++ty)
+                    for (const SlabRef& e : refs[((size_t)l * nzc + zc) * nty + ty]) {
+                        if (host_out && rows < cap_rows) {
+                            int64_t* o = host_out + 7 * rows;
+                            o[0] = c.gid[l];
+                            o[1] = zc;
+                            o[2] = ty;
+                            o[3] = e.rank;
+                            o[4] = c.plan.by_rank[e.rank][e.local];
+                            o[5] = e.zc;
+                            o[6] = e.ty;
+                        }
+                        ++rows;
+                    }
+        *n_rows = rows;
+        return J3D_OK;
+    });
+}
+
 int jacobi3d_nccl_unique_id(uint8_t out[128]) {
     return guarded([&]() -> int {
         if (!out) return fail(J3D_EINVAL, "out is NULL");
@@ -145,7 +185,7 @@ int jacobi3d_create(const jacobi3d_config* cfg, const uint8_t* nccl_uid, jacobi3
         CK(cudaMemset(c->arena + c->off_faces, 0, (size_t)(c->arena_bytes - c->off_faces)));
         CK(cudaMalloc(&c->d_descs, sizeof(StencilDesc) * 2 * c->n_local));
         CK(cudaMalloc(&c->d_tmaps, sizeof(CUtensorMap) * 2 * c->n_local));
-        CK(cudaMalloc(&c->d_tmaps_split, sizeof(CUtensorMap) * 4 * c->n_local));
+        CK(cudaMalloc(&c->d_tmaps_pro, sizeof(CUtensorMap) * 12 * c->n_local));
         CK(cudaMalloc(&c->d_tmaps_x, sizeof(CUtensorMap) * 2 * c->n_local));
         CK(cudaMalloc(&c->d_pack, sizeof(CopyDesc) * 12 * c->n_local));
         CK(cudaMalloc(&c->d_unpack, sizeof(CopyDesc) * 12 * c->n_local));
@@ -166,6 +206,7 @@ int jacobi3d_create(const jacobi3d_config* cfg, const uint8_t* nccl_uid, jacobi3
         c->peer_base.assign(c->n_gpus, nullptr);
         build_static_tables(c);
         build_tables(c);
+        CK(preload_kernels(c->tile_kind));
         CK(cudaStreamCreateWithFlags(&c->main, cudaStreamNonBlocking));
         int lo_pr = 0, hi_pr = 0;
         CK(cudaDeviceGetStreamPriorityRange(&lo_pr, &hi_pr));
@@ -198,19 +239,30 @@ int jacobi3d_create(const jacobi3d_config* cfg, const uint8_t* nccl_uid, jacobi3
         mk(&c->ev_fork);
         CK(cudaEventCreate(&c->ev_t0));
         CK(cudaEventCreate(&c->ev_t1));
+        CK(cudaHostAlloc((void**)&c->host_scratch, 64, cudaHostAllocDefault));
         if (c->n_gpus > 1) {
-            ncclUniqueId id;
-            std::memcpy(&id, nccl_uid, 128);
-            NK(ncclCommInitRank(&c->comm, c->n_gpus, id, c->rank));
             uint64_t h = 1469598103934665603ULL;  // FNV-1a of the unique id: a job-wide key
             for (int i = 0; i < 128; ++i) h = (h ^ nccl_uid[i]) * 1099511628211ULL;
             c->job_key = h;
+            // NCCL only where halos travel through it; the P2P and host-staging
+            // backends use the shared-memory control plane (control.cu)
+            if (cfg->exchange == J3D_XCHG_NCCL) {
+                ncclUniqueId id;
+                std::memcpy(&id, nccl_uid, 128);
+                NK(ncclCommInitRank(&c->comm, c->n_gpus, id, c->rank));
+            } else {
+                c->ctl_needed = true;
+                ctl_setup_own(c);
+            }
         }
         if (c->host_needed) {
             g_drv.load();
             host_setup_own(c);
         }
-        CK(cudaDeviceSynchronize());
+        // the arena memsets and table copies ran on the legacy stream; never a
+        // device-wide wait (ranks may share this GPU, see sync_streams)
+        CK(cudaStreamSynchronize(0));
+        CK(cudaStreamSynchronize(c->main));
         *out = c;
         return J3D_OK;
     });
@@ -233,7 +285,13 @@ int jacobi3d_ipc_export(jacobi3d_t* c, uint8_t* host_out, size_t cap, size_t* le
         r.rank = c->rank;
         r.device = c->device;
         r.arena_bytes = (uint64_t)c->arena_bytes;
+        r.process = process_token();
+        r.arena_ptr = (uint64_t)(uintptr_t)c->arena;
         CK(cudaSetDevice(c->device));
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, c->device));
+        static_assert(sizeof(prop.uuid) == 16, "uuid size");
+        std::memcpy(r.uuid, &prop.uuid, 16);
         if (c->p2p_needed) CK(cudaIpcGetMemHandle(&r.handle, c->arena));
         std::memcpy(host_out, &r, sizeof r);
         return J3D_OK;
@@ -243,31 +301,65 @@ int jacobi3d_ipc_export(jacobi3d_t* c, uint8_t* host_out, size_t cap, size_t* le
 int jacobi3d_ipc_connect(jacobi3d_t* c, const uint8_t* all, size_t len_per_rank) {
     return guarded([&]() -> int {
         if (!c || !all) return fail(J3D_EINVAL, "NULL argument");
-        if (c->host_needed && !c->host_connected) {
-            CK(cudaSetDevice(c->device));
-            host_connect(c);
-        }
-        if (!c->p2p_needed) return J3D_OK;
+        if (c->n_gpus == 1) return J3D_OK;
         if (len_per_rank != sizeof(IpcRecord)) return fail(J3D_EINVAL, "record size mismatch");
         CK(cudaSetDevice(c->device));
-        for (int r : c->peer_ranks) {
-            IpcRecord rec;
-            std::memcpy(&rec, all + (size_t)r * len_per_rank, sizeof rec);
-            if (rec.magic != kIpcMagic || rec.rank != r || rec.arena_bytes != (uint64_t)c->arena_bytes)
+        std::vector<IpcRecord> rec(c->n_gpus);
+        for (int r = 0; r < c->n_gpus; ++r) {
+            std::memcpy(&rec[r], all + (size_t)r * len_per_rank, sizeof(IpcRecord));
+            if (rec[r].magic != kIpcMagic || rec[r].rank != r || rec[r].arena_bytes != (uint64_t)c->arena_bytes)
                 return fail(J3D_EINVAL, "bad IPC record for rank " + std::to_string(r));
-            int can = 0;
-            cudaDeviceCanAccessPeer(&can, c->device, rec.device);
-            if (!can && rec.device != c->device)
-                return fail(J3D_EUNSUPPORTED, "device " + std::to_string(c->device) + " cannot access peer device " +
-                                                  std::to_string(rec.device));
-            void* p = nullptr;
-            CK(cudaIpcOpenMemHandle(&p, rec.handle, cudaIpcMemLazyEnablePeerAccess));
-            c->peer_base[r] = (char*)p;
         }
-        c->p2p_connected = true;
-        drop_graphs(c);
-        build_tables(c);
-        CK(cudaDeviceSynchronize());
+        // ranks on this GPU: threads of this process only.  Separate processes on
+        // one GPU are separate CUDA contexts that the GPU time-slices, and our
+        // cross-rank waits (epoch flags, persistent slab counters) need the ranks
+        // to run at the same time.
+        const IpcRecord& me = rec[c->rank];
+        c->co_resident = 0;
+        for (int r = 0; r < c->n_gpus; ++r) {
+            if (std::memcmp(rec[r].uuid, me.uuid, 16) != 0) continue;
+            c->co_resident += 1;
+            if (rec[r].process != me.process && c->cfg.exchange != J3D_XCHG_NCCL)
+                return fail(J3D_EUNSUPPORTED, "ranks " + std::to_string(c->rank) + " and " + std::to_string(r) +
+                                                  " share a GPU from different processes; run ranks that share a "
+                                                  "GPU as threads of one process (dist.ThreadGroup)");
+        }
+        c->persist_grid = std::max(1, c->grid_cap / std::max(1, c->co_resident));
+        if (c->host_needed && !c->host_connected) host_connect(c);
+        if (c->ctl_needed && !c->ctl_connected) ctl_connect(c);
+        if (c->p2p_needed && !c->p2p_connected) {
+            c->peer_ipc.assign(c->n_gpus, 0);
+            for (int r : c->peer_ranks) {
+                const IpcRecord& pr = rec[r];
+                if (pr.device != c->device || pr.process != me.process) {
+                    int can = 0;
+                    CK(cudaDeviceCanAccessPeer(&can, c->device, pr.device));
+                    if (!can && std::memcmp(pr.uuid, me.uuid, 16) != 0)
+                        return fail(J3D_EUNSUPPORTED, "device " + std::to_string(c->device) +
+                                                          " cannot access peer device " + std::to_string(pr.device));
+                }
+                if (pr.process == me.process) {  // a thread of this process: its arena address as is
+                    if (pr.device != c->device) {
+                        cudaError_t e = cudaDeviceEnablePeerAccess(pr.device, 0);
+                        if (e == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError();
+                        else CK(e);
+                    }
+                    c->peer_base[r] = (char*)(uintptr_t)pr.arena_ptr;
+                } else {
+                    void* p = nullptr;
+                    CK(cudaIpcOpenMemHandle(&p, pr.handle, cudaIpcMemLazyEnablePeerAccess));
+                    c->peer_base[r] = (char*)p;
+                    c->peer_ipc[r] = 1;
+                }
+            }
+            c->p2p_connected = true;
+            drop_graphs(c);
+            build_tables(c);
+        }
+        CK(cudaStreamSynchronize(0));
+        CK(cudaStreamSynchronize(c->main));
+        // every rank connected before any rank enqueues work that waits on a peer
+        ctl_barrier(c);
         return J3D_OK;
     });
 }
@@ -277,8 +369,9 @@ int jacobi3d_init(jacobi3d_t* c, int kind, const double* p, uint64_t seed) {
         if (!c) return fail(J3D_EINVAL, "ctx is NULL");
         if (kind < J3D_INIT_DEFAULT || kind > J3D_INIT_HASH) return fail(J3D_EINVAL, "unknown init kind");
         if ((kind == J3D_INIT_CONST || kind == J3D_INIT_LINEAR) && !p) return fail(J3D_EINVAL, "params required");
-        if ((c->p2p_needed && !c->p2p_connected) || (c->host_needed && !c->host_connected))
-            return fail(J3D_ESTATE, "P2P / host exchange needs jacobi3d_ipc_export/jacobi3d_ipc_connect first");
+        if ((c->p2p_needed && !c->p2p_connected) || (c->host_needed && !c->host_connected) ||
+            (c->ctl_needed && !c->ctl_connected))
+            return fail(J3D_ESTATE, "a multi-GPU context needs jacobi3d_ipc_export/jacobi3d_ipc_connect first");
         CK(cudaSetDevice(c->device));
         double pp[4] = {0, 0, 0, 0};
         if (p) std::memcpy(pp, p, sizeof pp);
@@ -414,8 +507,7 @@ int jacobi3d_synchronize(jacobi3d_t* c) {
     return guarded([&]() -> int {
         if (!c) return fail(J3D_EINVAL, "ctx is NULL");
         CK(cudaSetDevice(c->device));
-        wait_stream(c, c->main);
-        CK(cudaDeviceSynchronize());
+        sync_streams(c);
         if (c->comm) {
             ncclResult_t ar = ncclSuccess;
             NK(ncclCommGetAsyncError(c->comm, &ar));
@@ -434,10 +526,13 @@ int jacobi3d_residual(jacobi3d_t* c, double* out) {
         CK(cudaMemsetAsync(acc, 0, 8, c->main));
         CK(launch_residual(c->d_geom, c->n_local, (int)(c->iter & 1), acc, c->sms, c->main));
         count_launch(c, -1);
-        if (c->n_gpus > 1) NK(ncclAllReduce(acc, acc, 1, ncclUint64, ncclMax, c->comm, c->main));
-        unsigned long long h = 0;
-        CK(cudaMemcpyAsync(&h, acc, 8, cudaMemcpyDeviceToHost, c->main));
+        if (c->comm) NK(ncclAllReduce(acc, acc, 1, ncclUint64, ncclMax, c->comm, c->main));
+        // into pinned scratch, then the watchdog-polled wait (a pageable copy would
+        // block in the driver, past the watchdog, if a peer had stopped)
+        CK(cudaMemcpyAsync(c->host_scratch, acc, 8, cudaMemcpyDeviceToHost, c->main));
         wait_stream(c, c->main);
+        uint64_t h = c->host_scratch[0];
+        if (!c->comm) h = ctl_reduce(c, h, true);  // |differences| order like their bits; NaN wins
         double d;
         std::memcpy(&d, &h, 8);
         *out = d;
@@ -453,11 +548,12 @@ int jacobi3d_checksum(jacobi3d_t* c, uint64_t* out) {
         CK(cudaMemsetAsync(acc, 0, 8, c->main));
         CK(launch_checksum(c->d_geom, c->n_local, (int)(c->iter & 1), c->cfg.gx, c->cfg.gy, acc, c->sms, c->main));
         count_launch(c, -1);
-        if (c->n_gpus > 1) NK(ncclAllReduce(acc, acc, 1, ncclUint64, ncclSum, c->comm, c->main));
-        unsigned long long h = 0;
-        CK(cudaMemcpyAsync(&h, acc, 8, cudaMemcpyDeviceToHost, c->main));
+        if (c->comm) NK(ncclAllReduce(acc, acc, 1, ncclUint64, ncclSum, c->comm, c->main));
+        CK(cudaMemcpyAsync(c->host_scratch + 1, acc, 8, cudaMemcpyDeviceToHost, c->main));
         wait_stream(c, c->main);
-        *out = (uint64_t)h;
+        uint64_t h = c->host_scratch[1];
+        if (!c->comm) h = ctl_reduce(c, h, false);
+        *out = h;
         return J3D_OK;
     });
 }
@@ -467,9 +563,8 @@ int jacobi3d_time(jacobi3d_t* c, int64_t warmup, int64_t iters, double* ms) {
         if (!c || !ms || iters < 1 || warmup < 0) return fail(J3D_EINVAL, "bad argument");
         CK(cudaSetDevice(c->device));
         do_iterate(c, warmup);
-        wait_stream(c, c->main);
-        CK(cudaDeviceSynchronize());
-        nccl_barrier(c);
+        sync_streams(c);
+        ctl_barrier(c);
         CK(cudaEventRecord(c->ev_t0, c->main));
         do_iterate(c, iters);
         CK(cudaEventRecord(c->ev_t1, c->main));
@@ -493,6 +588,8 @@ int jacobi3d_get_stats(jacobi3d_t* c, jacobi3d_stats* out) {
         int64_t mx = 0;
         for (int64_t v : c->block_launches) mx = std::max(mx, v);
         out->launches_per_iter_block = c->stat_iters > 0 ? mx / c->stat_iters : 0;
+        out->tile_kind = c->tile_kind;
+        out->work_items = c->n_items;
         return J3D_OK;
     });
 }
@@ -509,7 +606,7 @@ int jacobi3d_profile_enable(jacobi3d_t* c, int enable) {
     return guarded([&]() -> int {
         if (!c) return fail(J3D_EINVAL, "ctx is NULL");
         CK(cudaSetDevice(c->device));
-        CK(cudaDeviceSynchronize());
+        sync_streams(c);
         for (auto& pr : c->prof_events) {
             c->ev_pool.push_back(pr.first);
             c->ev_pool.push_back(pr.second);
@@ -526,7 +623,7 @@ int jacobi3d_profile_read(jacobi3d_t* c, double* total_ms, int64_t* launches, do
     return guarded([&]() -> int {
         if (!c) return fail(J3D_EINVAL, "ctx is NULL");
         CK(cudaSetDevice(c->device));
-        CK(cudaDeviceSynchronize());
+        sync_streams(c);
         for (auto& pr : c->prof_events) {
             float f = 0;
             CK(cudaEventElapsedTime(&f, pr.first, pr.second));

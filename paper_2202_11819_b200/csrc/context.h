@@ -34,6 +34,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <mutex>
 #include <thread>
 #include <array>
 #include <cstdio>
@@ -84,7 +85,9 @@ struct Driver {
     fn_encode_tiled encode = nullptr;
     fn_write64 write64 = nullptr;
     fn_wait64 wait64 = nullptr;
-    void load() {
+    void load() {  // once per process; ranks may be threads of one process
+        static std::mutex m;
+        std::lock_guard<std::mutex> g(m);
         if (encode) return;
         cudaDriverEntryPointQueryResult q;
         void* p = nullptr;
@@ -108,13 +111,22 @@ static inline bool is_peer_kind(int k) { return k == PEER_NCCL || k == PEER_P2P 
 
 static inline int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
+// One rank's connection record (jacobi3d_ipc_export): the CUDA IPC handle of
+// its arena for peers in other processes, the raw arena address for peers in
+// the same process (ranks run as threads; an IPC handle cannot be opened in
+// the process that exported it), and the GPU's UUID, which tells ranks that
+// share a GPU apart from ranks on different GPUs.
 struct IpcRecord {
     uint64_t magic;
     int32_t rank, device;
-    uint64_t arena_bytes;
+    uint64_t arena_bytes;          // offset 16 (tests read it)
     cudaIpcMemHandle_t handle;
+    uint64_t process;              // process_token() of the exporting process
+    uint64_t arena_ptr;            // the arena's device address in that process
+    uint8_t uuid[16];              // cudaDeviceProp::uuid of the rank's GPU
 };
-static const uint64_t kIpcMagic = 0x4a33445f49504331ULL;  // "J3D_IPC1"
+static const uint64_t kIpcMagic = 0x4a33445f49504332ULL;  // "J3D_IPC2"
+uint64_t process_token();          // random, fixed for the life of the process
 
 }  // namespace j3d
 
@@ -140,7 +152,17 @@ struct jacobi3d {
     std::array<int64_t, 6> face_bytes{};
     int64_t faces_per_block_bytes = 0;
     std::vector<char*> peer_base;  // mapped arenas (index = rank), nullptr for self
+    std::vector<uint8_t> peer_ipc; // peer_base[r] was opened with cudaIpcOpenMemHandle (else same process)
     bool p2p_needed = false, p2p_connected = false;
+    // host control plane (n_gpus > 1 without an NCCL communicator, control.cu):
+    // one POSIX shared-memory segment per rank with a collective sequence
+    // number and two value slots -- barrier, sum and max over all ranks
+    bool ctl_needed = false, ctl_connected = false;
+    uint64_t ctl_seq = 0;
+    std::vector<char*> ctl_base;   // mapped segments (index = rank; own included)
+    int co_resident = 1;           // ranks of this job on this GPU (threads of one process)
+    int persist_grid = 0;          // persistent grid: grid_cap / co_resident (all co-resident ranks fit)
+    uint64_t* host_scratch = nullptr;  // pinned: residual / checksum results
     // host staging (J3D_XCHG_HOST): one POSIX shared-memory segment per rank,
     // [flags: 8 slots x n_gpus uint64 | staging: per local block, face, parity],
     // registered with CUDA so stream memory ops and DMA copies reach it
@@ -153,7 +175,7 @@ struct jacobi3d {
     // device tables
     StencilDesc* d_descs = nullptr;
     CUtensorMap* d_tmaps = nullptr;
-    CUtensorMap* d_tmaps_split = nullptr;
+    CUtensorMap* d_tmaps_pro = nullptr;  // [2*l + p][6] strategy C: maps over the receive buffers the prologue reads
     CUtensorMap* d_tmaps_x = nullptr;  // [2*l + p] x ghost vectors of each buffer
     int tma_mode = 0;
     WorkItem* d_items = nullptr;
@@ -273,6 +295,8 @@ FaceRef pack_dst(const jacobi3d* c, int l, int f, int par);
 void build_tables(jacobi3d* c);
 void build_static_tables(jacobi3d* c);
 void build_persist_deps(jacobi3d* c);
+struct SlabRef { int32_t rank, local, zc, ty; };  // slab (local block, z chunk, tile row) of a rank
+std::vector<std::vector<SlabRef>> slab_dep_refs(const jacobi3d* c, int nzc, int nty);
 
 // launch.cu
 cudaEvent_t pool_event(jacobi3d* c);
@@ -288,7 +312,15 @@ void drop_graphs(jacobi3d* c);
 void do_iterate(jacobi3d* c, int64_t n);
 void destroy_ctx(jacobi3d* c);
 void wait_stream(jacobi3d* c, cudaStream_t st);
-void nccl_barrier(jacobi3d* c);
+void sync_streams(jacobi3d* c);
+double timeout_s();
+
+// control.cu
+void ctl_setup_own(jacobi3d* c);
+void ctl_connect(jacobi3d* c);
+void ctl_teardown(jacobi3d* c);
+void ctl_barrier(jacobi3d* c);                         // every rank (NCCL all-reduce if a communicator exists)
+uint64_t ctl_reduce(jacobi3d* c, uint64_t v, bool max);  // sum / max over ranks of a host value (no communicator)
 
 // exchange.cu
 void nccl_exchange(jacobi3d* c, int par, cudaStream_t st);

@@ -41,8 +41,8 @@ struct StencilDesc {
     int32_t nx, ny, nz;
     uint32_t epi_mask;  // faces whose new boundary layer the epilogue stores to epi[f]
     int64_t pitch, zs;
-    uint32_t pro_mask;  // faces whose ghost values the prologue reads from pro[f]
-    uint32_t pad0;
+    uint32_t pro_mask;  // faces whose ghost values the prologue patches from pro[f] with generic loads
+    uint32_t pro_tma;   // faces whose ghost values the producer loads from pro[f] with TMA (strategy C)
     FaceRef epi[6];
     FaceRef pro[6];
 };

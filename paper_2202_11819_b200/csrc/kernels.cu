@@ -131,6 +131,14 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uin
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // Descriptor loads on rare paths: volatile so the compiler cannot hoist
 // them out of the plane loop (which would pin ~36 registers for the six
 // FaceRefs in the hot loop).
@@ -235,8 +243,17 @@ struct Tile {
     // SIDE_OFF + SIDE_STRIDE (TMA destinations are 128-byte aligned)
     static constexpr int SIDE_OFF = (W * H * 8 + 127) / 128 * 128;
     static constexpr int SIDE_STRIDE = (TY * 8 + 127) / 128 * 128;
-    static constexpr int STAGE_BYTES = SIDE_OFF + 2 * SIDE_STRIDE;
-    static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8 + 2 * 4 * 8 + 4 * 4 + 128;
+    // strategy C's y ghost rows, loaded from the receive buffers (-y at YSIDE_OFF,
+    // +y at YSIDE_OFF + YSIDE_STRIDE) and copied into the tile's ghost row by the
+    // warp that reads it
+    static constexpr int YSIDE_OFF = SIDE_OFF + 2 * SIDE_STRIDE;
+    static constexpr int YSIDE_STRIDE = (W * 8 + 127) / 128 * 128;
+    static constexpr int BAR_BYTES = 2 * NSTAGE * 8 + 2 * 4 * 8 + 4 * 4 + 128;
+    // the y side rows only where they keep MINB CTAs per SM (228 KB per SM, 1 KB
+    // reserved per CTA); otherwise strategy C patches y ghost rows generically
+    static constexpr bool YS = MINB * (NSTAGE * (YSIDE_OFF + 2 * YSIDE_STRIDE) + BAR_BYTES + 1024) <= 233472;
+    static constexpr int STAGE_BYTES = YS ? YSIDE_OFF + 2 * YSIDE_STRIDE : YSIDE_OFF;
+    static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + BAR_BYTES;
     static constexpr int THREADS = 32 * (NCW + 1);
     // the consumers hold the stages of planes z-1, z, z+1; at least one more is in flight
     static_assert((MAP == 1 ? TX % 32 : TX % 64) == 0 && W <= 256 && H <= 256 && NSTAGE >= 4, "tile shape");
@@ -351,7 +368,7 @@ __device__ __forceinline__ void epi_store(const StencilDesc* __restrict__ d, uin
 template <class T>
 __global__ void __launch_bounds__(T::THREADS, T::MINB)
     stencil_tma_kernel(const StencilDesc* __restrict__ descs, const CUtensorMap* __restrict__ tmaps,
-                       const CUtensorMap* __restrict__ tmaps3, const CUtensorMap* __restrict__ tmapsx,
+                       const CUtensorMap* __restrict__ tmapsp, const CUtensorMap* __restrict__ tmapsx,
                        const WorkItem* __restrict__ items, int n_items, int parity, int flags,
                        unsigned int* __restrict__ sched, const IterCtl ctl) {
     constexpr int NCW = T::NCW, RPW = T::RPW, CPL = T::CPL, W = T::W, NSTAGE = T::NSTAGE, IQ = 4;
@@ -407,28 +424,48 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                 const CUtensorMap* tx = tmapsx + bp;
                 tmap_acquire(tm);
                 tmap_acquire(tx);
-                const int nxb = descs[bp].nx;
+                const int nxb = descs[bp].nx, nyb = descs[bp].ny, nzb = descs[bp].nz;
+                // strategy C: ghost values the prologue takes from the receive buffers,
+                // loaded here with TMA ("unpack ... in one kernel"): the
+                // x ghost vectors, the y ghost rows (into the stage's y side rows) and
+                // whole ghost planes, from maps over the receive buffers (setup.cu)
+                const uint32_t ptma = (flags & 1) ? descs[bp].pro_tma : 0u;
+                const CUtensorMap* pm = tmapsp + 6 * bp;
                 // tiles at a block x edge also load the x ghost vectors of their rows
                 const uint32_t xe = (w.tx == 0 ? 1u : 0u) | ((w.tx + 1) * T::TX >= nxb ? 2u : 0u);
-                const uint32_t bytes = T::TX_BYTES + (uint32_t)__popc(xe) * (T::TY * 8);
+                const uint32_t ye = (ptma & 4u) && w.ty == 0 ? 1u : 0u;
+                const uint32_t ye2 = (ptma & 8u) && (w.ty + 1) * T::TY >= nyb ? 1u : 0u;
+                const uint32_t bytes = T::TX_BYTES + (uint32_t)__popc(xe) * (T::TY * 8) + (ye + ye2) * (T::W * 8);
                 const int c0 = w.tx * T::TX - T::HX, c1 = w.ty * T::TY;
+                if (ptma) {
+                    for (int f = 0; f < 6; ++f)
+                        if (ptma & (1u << f)) tmap_acquire(pm + f);
+                }
                 for (int z = w.z0 - 1; z <= w.z1; ++z) {
                     mbar_wait(&empty[s], ph ^ 1);
                     mbar_expect_tx(&full[s], bytes);
                     unsigned char* dst = smem + s * T::STAGE_BYTES;
-                    if (xe & 1u) tma_load_3d(dst + T::SIDE_OFF, tx, &full[s], c1, z + 1, 0);
-                    if (xe & 2u) tma_load_3d(dst + T::SIDE_OFF + T::SIDE_STRIDE, tx, &full[s], c1, z + 1, 1);
-                    if (tma_mode == 0) {
+                    // receive buffers: x faces (y, z), y faces (x, z), z faces (x, y), owned
+                    // coordinates only (ghost-plane / corner coordinates are zero-filled, unused)
+                    if (xe & 1u) {
+                        if (ptma & 1u) tma_load_2d(dst + T::SIDE_OFF, pm + 0, &full[s], c1, z);
+                        else tma_load_3d(dst + T::SIDE_OFF, tx, &full[s], c1, z + 1, 0);
+                    }
+                    if (xe & 2u) {
+                        if (ptma & 2u) tma_load_2d(dst + T::SIDE_OFF + T::SIDE_STRIDE, pm + 1, &full[s], c1, z);
+                        else tma_load_3d(dst + T::SIDE_OFF + T::SIDE_STRIDE, tx, &full[s], c1, z + 1, 1);
+                    }
+                    if constexpr (T::YS) {
+                        if (ye) tma_load_2d(dst + T::YSIDE_OFF, pm + 2, &full[s], c0, z);
+                        if (ye2) tma_load_2d(dst + T::YSIDE_OFF + T::YSIDE_STRIDE, pm + 3, &full[s], c0, z);
+                    }
+                    const int zf = z < 0 ? 4 : z >= nzb ? 5 : -1;
+                    if (zf >= 0 && (ptma & (1u << zf))) {
+                        tma_load_2d(dst, pm + zf, &full[s], c0, c1 - 1);  // the ghost plane: neighbour's face
+                    } else if (tma_mode == 0) {
                         tma_load_3d(dst, tm, &full[s], c0, c1, z + 1);
-                    } else if (tma_mode == 1 || tma_mode == 2) {
-                        tma_load_3d_hint(dst, tm, &full[s], c0, c1, z + 1, tma_mode == 1 ? pol_first : pol_last);
                     } else {
-                        // the two rows at each end of the box are shared with the
-                        // y-neighbour tiles: keep them (evict_last); stream the rest
-                        const CUtensorMap* t2 = tmaps3 + 2 * (2 * w.blk + (parity ^ (k & 1)));
-                        tma_load_3d_hint(dst, t2, &full[s], c0, c1, z + 1, pol_last);
-                        tma_load_3d_hint(dst + 2 * T::W * 8, t2 + 1, &full[s], c0, c1 + 2, z + 1, pol_first);
-                        tma_load_3d_hint(dst + (T::H - 2) * T::W * 8, t2, &full[s], c0, c1 + T::H - 2, z + 1, pol_last);
+                        tma_load_3d_hint(dst, tm, &full[s], c0, c1, z + 1, tma_mode == 1 ? pol_first : pol_last);
                     }
                     if (++s == NSTAGE) { s = 0; ph ^= 1; }
                 }
@@ -465,7 +502,8 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
         const int x0 = w.tx * T::TX, y0 = w.ty * T::TY;
         const int xl = x0 + (T::MAP == 1 ? lane : 2 * lane), yl = y0 + warp * RPW;  // this thread's first cell
         double* obase = d->out + (int64_t)(yl + 1) * pitch + XOFF + xl;
-        const uint32_t pro = faces ? d->pro_mask : 0u;
+        const uint32_t pro = faces ? d->pro_mask : 0u;   // ghost faces patched with generic loads (fallback)
+        const uint32_t ptma = faces ? d->pro_tma : 0u;   // ghost faces the producer loaded from receive buffers
         const uint32_t epi = faces ? d->epi_mask : 0u;
         // block faces (bits 0..3 = -x,+x,-y,+y) this tile's cells touch
         const uint32_t touch = (x0 == 0 ? 1u : 0u) | (x0 + T::TX >= nx ? 2u : 0u) | (y0 == 0 ? 4u : 0u) |
@@ -498,6 +536,12 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
         const bool xrf = (touch & 2u) && lane == (xlast_t & 31);
         const int xlb = T::SIDE_OFF / 8 + warp * RPW - sbase;
         const int xrb = (T::SIDE_OFF + T::SIDE_STRIDE) / 8 + warp * RPW - sbase - 32 * kedge;
+        // strategy C, y ghost rows from the receive buffers (TMA-fed): the warp
+        // reading the tile's -y ghost row (warp 0, tile row 0) / +y ghost row (the
+        // warp owning the block's last row) copies the stage's y side row into it
+        const int gly = ny - y0;  // tile-local row of the +y ghost
+        const bool ycopy_lo = (ptma & 4u) && y0 == 0 && warp == 0;
+        const bool ycopy_hi = (ptma & 8u) && gly <= T::TY && gly - 1 >= warp * RPW && gly - 1 < warp * RPW + RPW;
         auto acquire = [&](int zz) {
             mbar_wait(&full[s], ph);
             if (T::MAP == 0 && (touch & 3u)) {
@@ -507,6 +551,15 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                     if (touch & 2u) st[edr] = st[esr];
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 }
+                __syncwarp();
+            }
+            if (T::YS && (ycopy_lo | ycopy_hi)) {
+                double* st = stage(s);
+                for (int i = lane; i < T::TX; i += 32) {
+                    if (ycopy_lo) st[T::HX + i] = st[T::YSIDE_OFF / 8 + T::HX + i];
+                    if (ycopy_hi) st[(gly + 1) * W + T::HX + i] = st[(T::YSIDE_OFF + T::YSIDE_STRIDE) / 8 + T::HX + i];
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
             }
             if ((pro & touch) || (zz < 0 && (pro & 16u)) || (zz >= nz && (pro & 32u))) {
@@ -1050,7 +1103,7 @@ static cudaError_t launch_t(const StencilLaunch& L, cudaStream_t st) {
     }
     if (L.n_items <= 0) return cudaSuccess;
     stencil_tma_kernel<T><<<L.grid, T::THREADS, T::SMEM_BYTES, st>>>(
-        L.descs, L.tmaps, L.tmaps_split, L.tmaps_x, L.items, L.n_items, L.parity,
+        L.descs, L.tmaps, L.tmaps_pro, L.tmaps_x, L.items, L.n_items, L.parity,
         (L.faces ? 1 : 0) | ((L.tma_mode & 3) << 2), L.sched, L.ctl);
     return cudaGetLastError();
 }
@@ -1095,6 +1148,47 @@ cudaError_t stencil_occupancy(int kind, bool, int* blocks_per_sm) {
 #undef X
     }
     return cudaErrorInvalidValue;
+}
+
+// Load every kernel a context may launch now, at create time.  CUDA's lazy
+// module loading would otherwise load a kernel at its first launch, and that
+// load waits for kernels already running on the device -- a deadlock when a
+// running kernel waits for another rank on the same GPU (a persistent launch
+// spinning on a peer's slab counters while this rank's first end-of-call
+// wait kernel is being loaded).
+template <class T>
+static cudaError_t preload_t() {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaFuncGetAttributes(&a, stencil_tma_kernel<T>);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(stencil_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM_BYTES);
+}
+
+cudaError_t preload_kernels(int kind) {
+    cudaError_t e = cudaErrorInvalidValue;
+    switch (kind) {
+#define X(k, tx, ncw, rpw, ns, mb) \
+    case k: e = preload_t<J3D_TYPE(k, tx, ncw, rpw, ns, mb)>(); break;
+        J3D_TILES(X)
+#undef X
+    }
+    if (e != cudaSuccess) return e;
+    cudaFuncAttributes a;
+    const void* fns[] = {(const void*)wait_counters_kernel, (const void*)copy_faces_kernel, (const void*)init_kernel,
+                         (const void*)checksum_kernel, (const void*)residual_kernel};
+    for (const void* f : fns)
+        if ((e = cudaFuncGetAttributes(&a, f)) != cudaSuccess) return e;
+    return cudaSuccess;
+}
+
+bool tile_yside(int kind) {
+    switch (kind) {
+#define X(k, tx, ncw, rpw, ns, mb) \
+    case k: return J3D_TYPE(k, tx, ncw, rpw, ns, mb)::YS;
+        J3D_TILES(X)
+#undef X
+    }
+    return false;
 }
 
 int stencil_box_w(int kind) { return tile_shape(kind).tx + 8; }

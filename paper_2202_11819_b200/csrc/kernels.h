@@ -17,9 +17,9 @@ struct TileShape {
 struct StencilLaunch {
     const StencilDesc* descs;  // device, [2*n_local_blocks]
     const CUtensorMap* tmaps;  // device, [2*n_local_blocks], 64-B aligned
-    const CUtensorMap* tmaps_split;  // device, [2*n_local_blocks][2]: box heights 2 and H-4 (tma_mode 3)
+    const CUtensorMap* tmaps_pro;    // device, [2*n_local_blocks][6]: strategy C's receive buffers per face
     const CUtensorMap* tmaps_x;      // device, [2*n_local_blocks]: x ghost vectors (y, z, side), box TY x 1 x 1
-    int tma_mode;            // 0 plain, 1 evict_first, 2 evict_last, 3 split rows (shared rows evict_last)
+    int tma_mode;            // 0 plain, 1 evict_first, 2 evict_last (L2 policy experiments)
     const WorkItem* items;     // device
     int n_items;
     int parity;  // input buffer parity
@@ -33,9 +33,11 @@ struct StencilLaunch {
 int num_tile_kinds();
 TileShape tile_shape(int kind);
 int stencil_box_w(int kind);
+bool tile_yside(int kind);  // the tile's stages carry y side rows (strategy C's TMA-fed y ghost rows)
 int stencil_box_h(int kind);
 cudaError_t launch_stencil(const StencilLaunch& L, cudaStream_t st);
 cudaError_t stencil_occupancy(int kind, bool faces, int* blocks_per_sm);
+cudaError_t preload_kernels(int kind);  // defeat lazy loading (see kernels.cu)
 cudaError_t launch_div7_selftest(uint64_t n, uint64_t seed, unsigned long long* bad, double* example, int sms,
                                  cudaStream_t st);
 cudaError_t launch_wait_counters(const unsigned int* const* ptrs, int n, uint32_t need, uint64_t limit_ns,

@@ -30,19 +30,14 @@ void count_launch(jacobi3d* c, int l) {
 // Limit for the persistent launch's on-device counter waits: the host-wait
 // watchdog's J3D_TIMEOUT_S (default 600 s), so a legitimately late peer rank
 // is waited for as long as the host would wait for it.
-static uint64_t wait_limit_ns() {
-    double s = 600.0;
-    if (const char* e = std::getenv("J3D_TIMEOUT_S")) s = std::atof(e);
-    if (!(s > 0)) s = 600.0;
-    return (uint64_t)(s * 1e9);
-}
+static uint64_t wait_limit_ns() { return (uint64_t)(timeout_s() * 1e9); }
 
 void stencil(jacobi3d* c, int begin, int count, int parity, cudaStream_t st, int l) {
     if (count <= 0) return;
     StencilLaunch L;
     L.descs = c->d_descs;
     L.tmaps = c->d_tmaps;
-    L.tmaps_split = c->d_tmaps_split;
+    L.tmaps_pro = c->d_tmaps_pro;
     L.tmaps_x = c->d_tmaps_x;
     L.tma_mode = c->tma_mode;
     L.items = c->d_items + begin;
@@ -58,7 +53,9 @@ void stencil(jacobi3d* c, int begin, int count, int parity, cudaStream_t st, int
         const bool remote = c->n_remote_done > 0 && !c->skip_exchange;
         L.ctl = IterCtl{c->d_item_slab, remote ? c->d_slab_deps : c->d_slab_deps_local, c->d_done, n_iter,
                         c->slab_target, c->persist_base, remote ? 1 : 0, wait_limit_ns()};
-        L.grid = c->grid_cap;
+        // ranks sharing this GPU (threads of one process) split it, so that every
+        // rank's persistent grid is resident at once: their items wait on each other
+        L.grid = c->persist_grid > 0 ? c->persist_grid : c->grid_cap;
     }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     const bool prof = c->prof && !c->capturing;
@@ -319,14 +316,17 @@ void do_iterate(jacobi3d* c, int64_t n) {
 void destroy_ctx(jacobi3d* c) {
     if (!c) return;
     cudaSetDevice(c->device);
-    cudaDeviceSynchronize();
+    try {
+        sync_streams(c);
+    } catch (...) {
+    }
     // collective (jacobi3d.h): once every rank is here no peer still touches this
     // rank's arena -- persistent launches read the peers' slab counters over NVLink
     // until their own last iteration -- so freeing it cannot fault a slower peer
     bool abort_comm = false;
-    if (c->n_gpus > 1 && c->comm) {
+    if (c->n_gpus > 1 && (c->comm || c->ctl_connected)) {
         try {
-            nccl_barrier(c);
+            ctl_barrier(c);
         } catch (...) {
             abort_comm = true;
         }
@@ -354,12 +354,14 @@ void destroy_ctx(jacobi3d* c) {
         else ncclCommDestroy(c->comm);
     }
     for (size_t r = 0; r < c->peer_base.size(); ++r)
-        if (c->peer_base[r]) cudaIpcCloseMemHandle(c->peer_base[r]);
+        if (c->peer_base[r] && r < c->peer_ipc.size() && c->peer_ipc[r]) cudaIpcCloseMemHandle(c->peer_base[r]);
     host_teardown(c);
+    ctl_teardown(c);
+    if (c->host_scratch) cudaFreeHost(c->host_scratch);
     if (c->main) cudaStreamDestroy(c->main);
     cudaFree(c->d_descs);
     cudaFree(c->d_tmaps);
-    cudaFree(c->d_tmaps_split);
+    cudaFree(c->d_tmaps_pro);
     cudaFree(c->d_tmaps_x);
     cudaFree(c->d_items);
     cudaFree(c->d_pack);
@@ -384,13 +386,18 @@ void destroy_ctx(jacobi3d* c) {
 // watchdog (J3D_TIMEOUT_S, default 600 s): a peer that never signals its
 // epoch (or an NCCL error) surfaces as J3D_ETIMEOUT / J3D_ENCCL instead of a
 // hang.
+double timeout_s() {
+    double s = 600.0;
+    if (const char* e = std::getenv("J3D_TIMEOUT_S")) s = std::atof(e);
+    return s > 0 ? s : 600.0;
+}
+
 void wait_stream(jacobi3d* c, cudaStream_t st) {
     if (c->n_gpus == 1) {
         CK(cudaStreamSynchronize(st));
         return;
     }
-    double limit = 600.0;
-    if (const char* e = std::getenv("J3D_TIMEOUT_S")) limit = std::atof(e);
+    const double limit = timeout_s();
     const auto t0 = std::chrono::steady_clock::now();
     int us = 20;
     for (;;) {
@@ -412,11 +419,15 @@ void wait_stream(jacobi3d* c, cudaStream_t st) {
     }
 }
 
-void nccl_barrier(jacobi3d* c) {
-    if (c->n_gpus == 1 || !c->comm) return;
-    double* s = (double*)(c->arena + c->off_scratch + 64);
-    NK(ncclAllReduce(s, s, 1, ncclFloat64, ncclSum, c->comm, c->main));
-    wait_stream(c, c->main);
+// Wait for every stream of this context -- never cudaDeviceSynchronize: ranks
+// that are threads of one process share the device, and a device-wide wait
+// would also wait for a peer's queued work, which may itself wait for this
+// rank's next call (a deadlock).
+void sync_streams(jacobi3d* c) {
+    if (c->main) wait_stream(c, c->main);
+    for (auto s : c->lo) if (s) wait_stream(c, s);
+    for (auto s : c->hi) if (s) wait_stream(c, s);
+    if (c->xstream) wait_stream(c, c->xstream);
 }
 
 

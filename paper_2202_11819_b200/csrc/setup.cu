@@ -98,11 +98,32 @@ FaceRef pack_dst(const jacobi3d* c, int l, int f, int par) {
     return c->contiguous(c->face_buf(l, f, par, false), f);
 }
 
+// TMA map over a contiguous receive buffer of face f (layout: x faces (y, z),
+// y faces (x, z), z faces (x, y); owned coordinates).  Boxes: an x ghost
+// vector (TY x 1), a y ghost row (W x 1), a ghost plane (W x (TY+2)) -- the
+// shapes the stencil's stage expects (kernels.cu stencil_tma_kernel).
+static void encode_recv_map(const jacobi3d* c, CUtensorMap* m, const double* p, int f) {
+    const int tk = c->tile_kind;
+    const cuuint64_t na = (cuuint64_t)c->face_na(f), nb = (cuuint64_t)c->face_nb(f);
+    cuuint64_t dims[2] = {na, nb};
+    cuuint64_t strides[1] = {na * 8};
+    cuuint32_t box[2];
+    if (f < 2) { box[0] = (cuuint32_t)tile_shape(tk).ty; box[1] = 1; }
+    else if (f < 4) { box[0] = (cuuint32_t)stencil_box_w(tk); box[1] = 1; }
+    else { box[0] = (cuuint32_t)stencil_box_w(tk); box[1] = (cuuint32_t)stencil_box_h(tk); }
+    cuuint32_t es[2] = {1, 1};
+    DK(g_drv.encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(p), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+}
+
 void build_tables(jacobi3d* c) {
     const int nl = c->n_local;
     const int v = c->cfg.variant;
-    // ---- stencil descriptors [2*l + p]
+    // ---- stencil descriptors [2*l + p]; strategy C's receive-buffer maps [(2*l + p)*6 + f]
     std::vector<StencilDesc> descs(2 * nl);
+    std::vector<CUtensorMap> pro_maps((size_t)2 * nl * 6);
+    std::memset(pro_maps.data(), 0, pro_maps.size() * sizeof(CUtensorMap));
     c->faces_fused = false;
     for (int l = 0; l < nl; ++l)
         for (int p = 0; p < 2; ++p) {
@@ -147,13 +168,24 @@ void build_tables(jacobi3d* c) {
                         d.epi[f] = pack_dst(c, l, f, q);
                         d.epi_mask |= 1u << f;
                         d.pro[f] = recv_src(c, l, f, p);
-                        d.pro_mask |= 1u << f;
+                        // the producer loads these ghosts with TMA from the receive buffer when
+                        // its row stride is a multiple of 16 bytes (TMA); else the consumer
+                        // warps patch them with generic loads (patch_stage)
+                        const int64_t pitch_elems = c->face_na(f);
+                        const bool room = !(f == 2 || f == 3) || tile_yside(c->tile_kind);
+                        if (room && pitch_elems % 2 == 0 && ((uintptr_t)d.pro[f].p & 15) == 0) {
+                            d.pro_tma |= 1u << f;
+                            encode_recv_map(c, &pro_maps[(size_t)(2 * l + p) * 6 + f], d.pro[f].p, f);
+                        } else {
+                            d.pro_mask |= 1u << f;
+                        }
                     }
                 }
-                if (d.epi_mask | d.pro_mask) c->faces_fused = true;
+                if (d.epi_mask | d.pro_mask | d.pro_tma) c->faces_fused = true;
             }
         }
     CK(cudaMemcpy(c->d_descs, descs.data(), descs.size() * sizeof(StencilDesc), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_tmaps_pro, pro_maps.data(), pro_maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
 
     // ---- pack / unpack copy descriptors [(q*nl + l)*6 + f]
     std::vector<CopyDesc> pack(2 * nl * 6), unpack(2 * nl * 6);
@@ -250,54 +282,70 @@ void build_tables(jacobi3d* c) {
 // wrote -- and by symmetry of the 7-point neighbourhood exactly those slabs
 // read, in the previous iteration, the cells its own stores overwrite.
 // (Diagonal neighbours' corner cells are fetched by the TMA box but never
-// used.)  A neighbour on a peer GPU is named by a pointer into that rank's
-// IPC-mapped arena (remote counters), known only after jacobi3d_ipc_connect;
-// `remote` collects those pointers for the end-of-call wait.  The second
-// table drops every remote entry (timing with the exchange elided,
-// jacobi3d_set_skip_exchange).
-void build_persist_deps(jacobi3d* c) {
-    if (c->cfg.launch != J3D_PERSISTENT) return;
-    const int nl = c->n_local, nzc = c->persist_nzc, nty = c->persist_nty;
-    auto sid = [&](int l, int zc, int ty) { return ((int64_t)l * nzc + zc) * nty + ty; };
-    std::vector<const unsigned int*> deps((size_t)c->n_slabs * MAX_DEPS, nullptr), local(deps);
-    std::vector<const unsigned int*> remote;
-    // counter of slab (zc, ty) of the neighbour across face f of block l
-    auto counter = [&](int l, int f, int zc, int ty) -> const unsigned int* {
-        if (c->kind[l][f] == LOCAL) return c->d_done + sid(c->nbr_local[l][f], zc, ty);
-        if (c->kind[l][f] != PEER_P2P || !c->p2p_connected) return nullptr;
-        const int r = c->plan.blocks[c->plan.blocks[c->gid[l]].nbr[f]].owner;
-        const uintptr_t p = (uintptr_t)((const unsigned int*)(c->peer_base[r] + c->off_done) +
-                                        sid(c->nbr_local[l][f], zc, ty));
-        return (const unsigned int*)(p | 1);  // tag: system-scope acquire (device.cuh)
+// used.)  slab_dep_refs lists them symbolically (rank, local block, zc,
+// ty) -- jacobi3d_debug_slab_deps exports that list without a GPU, and
+// tests/test_persistent_rule.py checks it against the brute-force hazard set.
+std::vector<std::vector<SlabRef>> slab_dep_refs(const jacobi3d* c, int nzc, int nty) {
+    const int nl = c->n_local;
+    std::vector<std::vector<SlabRef>> out((size_t)nl * nzc * nty);
+    // slab (zc, ty) of the neighbour across face f of block l; none for a
+    // Dirichlet face or a peer face whose halo does not travel by P2P stores
+    auto across = [&](int l, int f, int zc, int ty, std::vector<SlabRef>& d) {
+        const int k = c->kind[l][f];
+        if (k != LOCAL && k != PEER_P2P) return;
+        const int r = k == LOCAL ? c->rank : c->plan.blocks[c->plan.blocks[c->gid[l]].nbr[f]].owner;
+        d.push_back(SlabRef{r, c->nbr_local[l][f], zc, ty});
     };
     for (int l = 0; l < nl; ++l)
         for (int zc = 0; zc < nzc; ++zc)
             for (int ty = 0; ty < nty; ++ty) {
-                const unsigned int** d = &deps[(size_t)sid(l, zc, ty) * MAX_DEPS];
-                const unsigned int** dl = &local[(size_t)sid(l, zc, ty) * MAX_DEPS];
-                int n = 0, nloc = 0;
-                auto add = [&](const unsigned int* p, bool is_local) {
-                    if (!p) return;
-                    if (n == MAX_DEPS) throw Error(J3D_EUNSUPPORTED, "slab dependency table overflow");
-                    d[n++] = p;
-                    if (is_local) dl[nloc++] = p;
-                    else if (std::find(remote.begin(), remote.end(), p) == remote.end()) remote.push_back(p);
-                };
-                add(c->d_done + sid(l, zc, ty), true);
-                if (zc > 0) add(c->d_done + sid(l, zc - 1, ty), true);
-                if (zc + 1 < nzc) add(c->d_done + sid(l, zc + 1, ty), true);
-                if (ty > 0) add(c->d_done + sid(l, zc, ty - 1), true);
-                if (ty + 1 < nty) add(c->d_done + sid(l, zc, ty + 1), true);
-                for (int f = 0; f < 2; ++f) add(counter(l, f, zc, ty), c->kind[l][f] == LOCAL);
-                if (ty == 0) add(counter(l, 2, zc, nty - 1), c->kind[l][2] == LOCAL);
-                if (ty == nty - 1) add(counter(l, 3, zc, 0), c->kind[l][3] == LOCAL);
-                if (zc == 0) add(counter(l, 4, nzc - 1, ty), c->kind[l][4] == LOCAL);
-                if (zc == nzc - 1) add(counter(l, 5, 0, ty), c->kind[l][5] == LOCAL);
+                std::vector<SlabRef>& d = out[((size_t)l * nzc + zc) * nty + ty];
+                d.push_back(SlabRef{c->rank, l, zc, ty});
+                if (zc > 0) d.push_back(SlabRef{c->rank, l, zc - 1, ty});
+                if (zc + 1 < nzc) d.push_back(SlabRef{c->rank, l, zc + 1, ty});
+                if (ty > 0) d.push_back(SlabRef{c->rank, l, zc, ty - 1});
+                if (ty + 1 < nty) d.push_back(SlabRef{c->rank, l, zc, ty + 1});
+                for (int f = 0; f < 2; ++f) across(l, f, zc, ty, d);
+                if (ty == 0) across(l, 2, zc, nty - 1, d);
+                if (ty == nty - 1) across(l, 3, zc, 0, d);
+                if (zc == 0) across(l, 4, nzc - 1, ty, d);
+                if (zc == nzc - 1) across(l, 5, 0, ty, d);
+                if (d.size() > (size_t)MAX_DEPS) throw Error(J3D_EUNSUPPORTED, "slab dependency table overflow");
             }
-    for (auto& p : remote) p = (const unsigned int*)((uintptr_t)p & ~uintptr_t(1));
+    return out;
+}
+
+// The tables the kernel reads: slab_dep_refs resolved to counter addresses
+// (a peer's through its IPC-mapped arena, tagged for a system-scope acquire;
+// known only after jacobi3d_ipc_connect).  `remote` collects the peer
+// counters for the end-of-call wait.  The second table drops every remote
+// entry (timing with the exchange elided, jacobi3d_set_skip_exchange).
+void build_persist_deps(jacobi3d* c) {
+    if (c->cfg.launch != J3D_PERSISTENT) return;
+    const int nzc = c->persist_nzc, nty = c->persist_nty;
+    auto sid = [&](int l, int zc, int ty) { return ((int64_t)l * nzc + zc) * nty + ty; };
+    const std::vector<std::vector<SlabRef>> refs = slab_dep_refs(c, nzc, nty);
+    std::vector<const unsigned int*> deps((size_t)c->n_slabs * MAX_DEPS, nullptr), local(deps);
+    std::vector<const unsigned int*> remote;
+    for (int64_t s = 0; s < (int64_t)refs.size(); ++s) {
+        int n = 0, nloc = 0;
+        for (const SlabRef& e : refs[s]) {
+            if (e.rank == c->rank) {
+                const unsigned int* p = c->d_done + sid(e.local, e.zc, e.ty);
+                deps[(size_t)s * MAX_DEPS + n++] = p;
+                local[(size_t)s * MAX_DEPS + nloc++] = p;
+            } else if (c->p2p_connected) {
+                const uintptr_t p = (uintptr_t)((const unsigned int*)(c->peer_base[e.rank] + c->off_done) +
+                                                sid(e.local, e.zc, e.ty));
+                deps[(size_t)s * MAX_DEPS + n++] = (const unsigned int*)(p | 1);  // tag: system scope (device.cuh)
+                if (std::find(remote.begin(), remote.end(), (const unsigned int*)p) == remote.end())
+                    remote.push_back((const unsigned int*)p);
+            }
+        }
+    }
     CK(cudaMemcpy(c->d_slab_deps, deps.data(), deps.size() * sizeof(void*), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->d_slab_deps_local, local.data(), local.size() * sizeof(void*), cudaMemcpyHostToDevice));
-    cudaFree(c->d_remote_done);
+    if (c->d_remote_done) cudaFree(c->d_remote_done);
     c->d_remote_done = nullptr;
     c->n_remote_done = (int)remote.size();
     if (!remote.empty()) {
@@ -366,23 +414,7 @@ void build_static_tables(jacobi3d* c) {
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
         }
     CK(cudaMemcpy(c->d_tmaps_x, xmaps.data(), xmaps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
-    // split maps: box heights 2 and H-4 (for the L2-policy split loads)
-    std::vector<CUtensorMap> maps2(4 * nl);
-    for (int l = 0; l < nl; ++l)
-        for (int p = 0; p < 2; ++p)
-            for (int h = 0; h < 2; ++h) {
-                cuuint64_t dims[3] = {(cuuint64_t)c->nx, (cuuint64_t)(c->ny + 2), (cuuint64_t)(c->nz + 2)};
-                cuuint64_t strides[2] = {(cuuint64_t)(c->pitch * 8), (cuuint64_t)(c->zs * 8)};
-                const int H = stencil_box_h(c->tile_kind);
-                cuuint32_t box[3] = {(cuuint32_t)stencil_box_w(c->tile_kind), (cuuint32_t)(h == 0 ? 2 : std::max(1, H - 4)), 1};
-                cuuint32_t es[3] = {1, 1, 1};
-                DK(g_drv.encode(&maps2[(2 * l + p) * 2 + h], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->buf(l, p) + XOFF, dims,
-                                strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
-                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
-            }
-    CK(cudaMemcpy(c->d_tmaps_split, maps2.data(), maps2.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
-    if (const char* e = std::getenv("J3D_TMA_HINT")) c->tma_mode = std::atoi(e) & 3;
-    if (c->tma_mode == 3 && stencil_box_h(c->tile_kind) < 6) c->tma_mode = 0;
+    if (const char* e = std::getenv("J3D_TMA_HINT")) c->tma_mode = std::atoi(e) % 3;
 
     // ---- work items: per block, z-chunk outer, then ty, tx (x fastest), peer-face blocks first
     int occ = 1;

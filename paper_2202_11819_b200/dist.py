@@ -49,3 +49,78 @@ def create(grid, odf=1, variant="direct", launch="batched", graph=False, exchang
         _, recs = bootstrap_bytes(lambda: None, ctx.ipc_export())
         ctx.ipc_connect(recs)
     return ctx
+
+
+class ThreadGroup:
+    """Ranks as threads of ONE process, sharing one GPU (or a few).
+
+    The same collective C ABI as the torchrun path -- every rank creates its
+    context, exports its connection record, connects, then calls the
+    collective API in the same order -- but the ranks are Python threads
+    (ctypes releases the GIL inside every library call) and their contexts
+    live in one CUDA context, so kernels and stream waits of different ranks
+    run concurrently.  Peers in the same process are mapped by address
+    instead of CUDA IPC, and the P2P / host-staging backends use the
+    library's shared-memory control plane (no NCCL, which refuses two ranks
+    on one GPU).  This is how the multi-rank paths (NVLink-style P2P stores,
+    epoch flags, host staging, overlap, persistent cross-rank counters, the
+    (2,2,2) eight-rank grid) run on a one-GPU machine.
+
+    Run with CUDA_DEVICE_MAX_CONNECTIONS=32 and at most ~30 library streams
+    in total (each rank: 1 main + 1 overlap + 2 per block in the per-block
+    launch mode), so that no rank's flag wait shares a hardware queue with
+    work another rank's flag depends on.
+    """
+
+    def __init__(self, n: int, device: int = 0, devices=None):
+        import threading
+
+        self.n = n
+        self.devices = list(devices) if devices is not None else [device] * n
+        self.uid = os.urandom(128)  # job key of the shared-memory control plane (no NCCL)
+        self._bar = threading.Barrier(n)
+        self._recs = [None] * n
+
+    def create(self, rank: int, grid, **kw):
+        """Collective over the group's threads: context + connection."""
+        from .jacobi3d import Jacobi3D
+
+        ctx = Jacobi3D(grid, n_gpus=self.n, rank=rank, device=self.devices[rank], nccl_uid=self.uid, **kw)
+        try:
+            self._recs[rank] = ctx.ipc_export()
+            self._bar.wait(timeout=600)
+            ctx.ipc_connect(list(self._recs))
+            self._bar.wait(timeout=600)
+        except BaseException:
+            self._bar.abort()
+            raise
+        return ctx
+
+    def barrier(self):
+        self._bar.wait(timeout=600)
+
+    def run(self, fn):
+        """fn(rank) on n threads; returns the per-rank results (re-raises the
+        first exception after every thread has finished)."""
+        import threading
+
+        out = [None] * self.n
+        err = [None] * self.n
+
+        def body(r):
+            try:
+                out[r] = fn(r)
+            except BaseException as e:  # noqa: BLE001 - reported below
+                err[r] = e
+                self._bar.abort()
+
+        ts = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(self.n)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        self._bar.reset()
+        for e in err:
+            if e is not None:
+                raise e
+        return out

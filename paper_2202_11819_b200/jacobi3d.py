@@ -45,7 +45,8 @@ class PlanInfo(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
                 ("graph_launches", ctypes.c_int64), ("last_graph_parity", ctypes.c_int64),
-                ("launches_per_iter_block", ctypes.c_int64)]
+                ("launches_per_iter_block", ctypes.c_int64), ("tile_kind", ctypes.c_int64),
+                ("work_items", ctypes.c_int64)]
 
 
 class Jacobi3DError(RuntimeError):
@@ -82,6 +83,7 @@ def _load():
         "jacobi3d_profile_enable": [P, ctypes.c_int],
         "jacobi3d_profile_read": [P, ctypes.POINTER(D), ctypes.POINTER(I64), ctypes.POINTER(D)],
         "jacobi3d_set_skip_exchange": [P, ctypes.c_int],
+        "jacobi3d_debug_slab_deps": [ctypes.POINTER(Config), I32, I32, P, I64, ctypes.POINTER(I64)],
         "jacobi3d_destroy": [P],
         "jacobi3d_div7_selftest": [U64, U64, ctypes.POINTER(U64), P],
     }
@@ -123,6 +125,17 @@ def plan(grid, odf=1, n_gpus=1, block=(0, 0, 0), rank=0, launch="batched") -> di
     return {"gpu_grid": tuple(info.gpu_grid), "blk_grid": tuple(info.blk_grid), "blk_ext": tuple(info.blk_ext),
             "n_blocks": info.n_blocks, "bytes_per_gpu": info.bytes_per_gpu,
             "peer_faces_max": info.peer_faces_max, "local_faces": info.local_faces}
+
+
+def debug_slab_deps(grid, odf=1, n_gpus=1, rank=0, tile_ty=1, nzc=1, block=(0, 0, 0)) -> np.ndarray:
+    """jacobi3d_debug_slab_deps (no GPU): the persistent launch's dependency
+    lists of one rank, rows (block, zc, ty, dep_rank, dep_block, dep_zc, dep_ty)."""
+    cfg = make_config(grid, odf=odf, n_gpus=n_gpus, rank=rank, block=block, launch="persistent")
+    n = ctypes.c_int64()
+    _ck(lib.jacobi3d_debug_slab_deps(ctypes.byref(cfg), tile_ty, nzc, None, 0, ctypes.byref(n)))
+    out = np.zeros((n.value, 7), dtype=np.int64)
+    _ck(lib.jacobi3d_debug_slab_deps(ctypes.byref(cfg), tile_ty, nzc, out.ctypes.data, n.value, ctypes.byref(n)))
+    return out
 
 
 def nccl_unique_id() -> bytes:

@@ -43,17 +43,30 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--bench")
     ap.add_argument("--note", default="")
+    ap.add_argument("--launch", required=True, help="launch mode of the captured run (bench.py --launch)")
+    ap.add_argument("--variant", default="direct")
+    ap.add_argument("--tile-kind", type=int, required=True, help="stats()['tile_kind'] of the captured run")
+    ap.add_argument("--iters-per-launch", type=int, default=1)
+    ap.add_argument("--alg-bytes", type=float, required=True, help="algorithmic bytes per captured launch")
+    ap.add_argument("--name", default=None, help="file suffix (default: the round)")
     a = ap.parse_args()
     s = summary(a.rep)[0]
     rd = to_bytes(*s["dram__bytes_read.sum"])
     wr = to_bytes(*s["dram__bytes_write.sum"])
     dur_ms = float(s["gpu__time_duration.sum"][0])
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    js = {"round": a.round, "workload": a.workload, "kernel": s.get("kernel"),
-          "traffic_bytes_per_launch": rd + wr, "dram_read_bytes": rd, "dram_write_bytes": wr,
+    import hashlib
+
+    with open(os.path.join(ROOT, "paper_2202_11819_b200", "libjacobi3d.so"), "rb") as f:
+        sha = hashlib.sha256(f.read()).hexdigest()  # the build the capture was taken with (bench.py checks it)
+    js = {"round": a.round, "workload": a.workload, "launch": a.launch, "variant": a.variant,
+          "tile_kind": a.tile_kind, "iters_per_launch": a.iters_per_launch, "lib_sha256": sha,
+          "kernel": s.get("kernel"), "traffic_bytes_per_launch": rd + wr, "dram_read_bytes": rd,
+          "dram_write_bytes": wr, "alg_bytes_per_launch": a.alg_bytes, "traffic_over_alg": (rd + wr) / a.alg_bytes,
           "ncu_duration_ms": dur_ms, "source": os.path.basename(a.rep),
           "metrics": {k: v for k, v in s.items() if k != "kernel"}}
-    with open(os.path.join(ROOT, "profiles", f"ncu_stencil_{a.round}.json"), "w") as f:
+    name = a.name or a.round
+    with open(os.path.join(ROOT, "profiles", f"ncu_stencil_{name}.json"), "w") as f:
         json.dump(js, f, indent=1)
     md = [f"# {a.round}: ncu evidence for the stencil ({a.workload})", "", a.note, "",
           "## `ncu --set full --clock-control none` of one stencil launch", "", "| metric | value | unit |",
@@ -63,7 +76,7 @@ def main():
             md.append(f"| {k} | {v[0]} | {v[1]} |")
     md += ["", f"kernel: `{s.get('kernel')}`", "",
            f"DRAM traffic per launch: read {rd/1e9:.3f} GB + write {wr/1e9:.3f} GB = {(rd+wr)/1e9:.3f} GB "
-           f"(algorithmic 16 B/LUP x 1536^3 = 57.982 GB)", ""]
+           f"(algorithmic {a.alg_bytes/1e9:.3f} GB: {(rd+wr)/a.alg_bytes:.4f}x)", ""]
     if a.launches:
         L = launches(a.launches)
         tot = sum(v for _, v in L)
@@ -77,7 +90,7 @@ def main():
         line = [l for l in open(a.bench) if l.startswith("{")]
         if line:
             md += ["## bench.py line of the same build", "", "```", line[-1].strip(), "```", ""]
-    with open(os.path.join(ROOT, "profiles", f"{a.round}_ncu_summary.md"), "w") as f:
+    with open(os.path.join(ROOT, "profiles", f"{name}_ncu_summary.md"), "w") as f:
         f.write("\n".join(md))
     print("wrote profiles for", a.round)
 

@@ -127,3 +127,4 @@ def test_binding_constants_match_header():
     for k, v in pairs.items():
         assert hdr.get(k) == v, (k, hdr.get(k), v)
     assert ctypes.sizeof(b.Config) == 8 * 6 + 4 * 10 + 8  # jacobi3d_config: 6 int64, 10 int32, 1 double
+    assert ctypes.sizeof(b.Stats) == 8 * 7  # jacobi3d_stats: 7 int64

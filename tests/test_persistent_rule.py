@@ -1,11 +1,11 @@
-"""The persistent launch's dependency rule, checked by brute force (CPU).
+"""The persistent launch's dependency tables, checked by brute force (CPU).
 
 J3D_PERSISTENT lets an item of iteration k start once the *slabs* (one tile
 row of one block over one z chunk) in its dependency list finished iteration
-k-1 (setup.cu build_persist_deps).  The rule lists, for slab
-(b, zc, ty): itself, (b, zc+-1, ty), (b, zc, ty+-1), the x neighbours'
-(zc, ty), for an edge tile row the y neighbour's edge row, for an edge chunk
-the z neighbour's edge chunk.
+k-1.  The lists are taken from the library itself
+(jacobi3d_debug_slab_deps: the same setup.cu slab_dep_refs that fills the
+device tables, local and peer-tagged entries) for 1-, 2-, 4- and 8-rank
+plans.
 
 Here every slab's cell sets are enumerated on small decompositions -- the
 cells it WRITES (its owned cells in the output buffer, plus the ghost cells
@@ -13,7 +13,7 @@ its direct-variant epilogue stores into the neighbours' output buffers) and
 the cells it READS (the 7-point neighbourhoods of its owned cells in the input
 buffer, ghosts included) -- and every hazard between consecutive iterations
 (RAW: k reads what k-1 wrote; WAR: k overwrites what k-1 read, in the same
-buffer because the two buffers alternate) must be covered by the rule, and
+buffer because the two buffers alternate) must be in the library's list, and
 every listed dependency must be a real hazard.
 """
 import itertools
@@ -74,38 +74,6 @@ def cell_sets(nb, ext, ty_, nzc):
     return sets
 
 
-def rule(nb, ext, ty_, nzc):
-    """The dependency rule of setup.cu build_persist_deps."""
-    nty, _ = slabs_of(nb, ext, ty_, nzc)
-    nbrs = neighbours(nb)
-    deps = {}
-    for b in nbrs:
-        for zc in range(nzc):
-            for t in range(nty):
-                d = {(b, zc, t)}
-                if zc > 0:
-                    d.add((b, zc - 1, t))
-                if zc + 1 < nzc:
-                    d.add((b, zc + 1, t))
-                if t > 0:
-                    d.add((b, zc, t - 1))
-                if t + 1 < nty:
-                    d.add((b, zc, t + 1))
-                for f in (0, 1):
-                    if nbrs[b][f] is not None:
-                        d.add((nbrs[b][f], zc, t))
-                if t == 0 and nbrs[b][2] is not None:
-                    d.add((nbrs[b][2], zc, nty - 1))
-                if t == nty - 1 and nbrs[b][3] is not None:
-                    d.add((nbrs[b][3], zc, 0))
-                if zc == 0 and nbrs[b][4] is not None:
-                    d.add((nbrs[b][4], nzc - 1, t))
-                if zc == nzc - 1 and nbrs[b][5] is not None:
-                    d.add((nbrs[b][5], 0, t))
-                deps[(b, zc, t)] = d
-    return deps
-
-
 def used(cells, ext):
     """Drop cells no 7-point stencil ever uses: edge / corner ghosts (two or
     more coordinates outside the owned range)."""
@@ -119,22 +87,58 @@ def used(cells, ext):
     return keep
 
 
-@pytest.mark.parametrize("nb,ext,ty_,nzc", [
-    ((2, 2, 2), (4, 6, 6), 2, 3),    # 8 blocks, 3 tile rows, 3 chunks
-    ((1, 3, 2), (3, 5, 4), 2, 2),    # ragged last tile row
-    ((2, 1, 1), (4, 4, 4), 4, 1),    # one tile row, one chunk per block
-    ((1, 1, 3), (2, 3, 1), 1, 1),    # 1-plane blocks: edge chunk on both sides
-    ((2, 2, 1), (3, 2, 5), 1, 5),    # 1-plane chunks, 1-row tiles
+def library_tables(grid, odf, n_gpus, ty_, nzc):
+    """The library's lists for every rank (jacobi3d_debug_slab_deps, the code
+    that fills the device tables), keyed by slab (block position, zc, ty),
+    plus the block grid, block extent and the owner rank of every block."""
+    from paper_2202_11819_b200 import jacobi3d as jb
+
+    info = jb.plan(grid, odf=odf, n_gpus=n_gpus)
+    nb = tuple(g * b for g, b in zip(info["gpu_grid"], info["blk_grid"]))
+    ext = tuple(info["blk_ext"])
+
+    def pos(i):  # block id: x-fastest on the global block grid (jacobi3d.h)
+        return (int(i) % nb[0], int(i) // nb[0] % nb[1], int(i) // (nb[0] * nb[1]))
+
+    deps, owner = {}, {}
+    for r in range(n_gpus):
+        rows = jb.debug_slab_deps(grid, odf=odf, n_gpus=n_gpus, rank=r, tile_ty=ty_, nzc=nzc)
+        for b, zc, t, dr, db, dzc, dt in rows.tolist():
+            key = (pos(b), zc, t)
+            assert owner.setdefault(pos(b), r) == r, "a block listed by two ranks"
+            deps.setdefault(key, set()).add((pos(db), dzc, dt, dr))
+    return nb, ext, deps, owner
+
+
+@pytest.mark.parametrize("grid,odf,n_gpus,ty_,nzc", [
+    ((8, 12, 12), 8, 1, 2, 3),     # 1 rank: 8 blocks 4x6x6, 3 tile rows, 3 chunks
+    ((3, 15, 8), 6, 1, 2, 2),      # ragged last tile row (5 rows, tiles of 2)
+    ((8, 4, 4), 2, 1, 4, 1),       # one tile row, one chunk per block
+    ((2, 3, 3), 3, 1, 1, 1),       # 1-plane blocks: an edge chunk on both sides
+    ((6, 2, 5), 4, 1, 1, 5),       # 1-plane chunks, 1-row tiles
+    ((8, 8, 8), 4, 2, 2, 2),       # 2 ranks: peer z faces
+    ((16, 6, 6), 4, 2, 3, 3),      # 2 ranks split along x: peer x faces
+    ((8, 8, 8), 1, 8, 2, 2),       # 8 ranks on the (2,2,2) grid: every face kind is a peer face
+    ((8, 12, 8), 2, 8, 2, 2),      # 8 ranks, 2 blocks each
+    ((12, 8, 8), 1, 4, 3, 2),      # 4 ranks (1,2,2)-like, ragged tile rows
 ])
-def test_rule_covers_exactly_the_hazards(nb, ext, ty_, nzc):
+def test_library_tables_equal_the_hazards(grid, odf, n_gpus, ty_, nzc):
+    """Every slab's list in the library's tables (local and peer-tagged entries,
+    from jacobi3d_debug_slab_deps) equals the set of slabs it has a hazard with
+    across consecutive iterations -- RAW (k reads what k-1 wrote) or WAR (k
+    overwrites what k-1 read) -- computed by brute force from the cell sets;
+    and an entry's rank is the owner of the listed block."""
+    nb, ext, deps, owner = library_tables(grid, odf, n_gpus, ty_, nzc)
     sets = cell_sets(nb, ext, ty_, nzc)
-    deps = rule(nb, ext, ty_, nzc)
+    assert set(deps) == set(sets), "the tables cover exactly the slabs of the decomposition"
     for s, (R, W) in sets.items():
         R = used(R, ext)
         need = set()
         for s2, (R2, W2) in sets.items():
-            R2 = used(R2, ext)
-            if R & W2 or W & R2:  # RAW (k reads what k-1 wrote) or WAR (k overwrites what k-1 read)
+            if R & W2 or W & used(R2, ext):
                 need.add(s2)
-        assert need <= deps[s], (s, sorted(need - deps[s]))
-        assert deps[s] <= need, (s, sorted(deps[s] - need))
+        got = {d[:3] for d in deps[s]}
+        assert len(got) == len(deps[s]), (s, "duplicate entries")
+        assert got == need, (s, sorted(need - got), sorted(got - need))
+        for d in deps[s]:
+            assert d[3] == owner[d[0]], (s, d)
