@@ -207,7 +207,10 @@ J3D_API int jacobi3d_create(const jacobi3d_config *cfg, const uint8_t *nccl_uid,
  * maps the neighbours' device memory (P2P), the neighbours' staging
  * segments (host backend) and every rank's control segment, and ends with a
  * barrier.  connect returns J3D_EUNSUPPORTED if ranks of different processes
- * share a GPU, or a P2P peer's GPU is not reachable.  n_gpus == 1: no-op. */
+ * share a GPU, if use_graph is set while some GPU hosts several ranks (graph
+ * launches of one CUDA context share its internal streams, so a captured
+ * epoch wait of one rank can block the peer work it waits for), or if a P2P
+ * peer's GPU is not reachable.  n_gpus == 1: no-op. */
 J3D_API int jacobi3d_ipc_export(jacobi3d_t *ctx, uint8_t *host_out, size_t cap, size_t *len);
 J3D_API int jacobi3d_ipc_connect(jacobi3d_t *ctx, const uint8_t *host_all, size_t len_per_rank);
 

@@ -324,6 +324,13 @@ int jacobi3d_ipc_connect(jacobi3d_t* c, const uint8_t* all, size_t len_per_rank)
                                                   " share a GPU from different processes; run ranks that share a "
                                                   "GPU as threads of one process (dist.ThreadGroup)");
         }
+        bool shared = false;  // some GPU of the job hosts more than one rank (the same answer on every rank)
+        for (int a = 0; a < c->n_gpus && !shared; ++a)
+            for (int b = a + 1; b < c->n_gpus && !shared; ++b) shared = std::memcmp(rec[a].uuid, rec[b].uuid, 16) == 0;
+        if (shared && c->cfg.use_graph)
+            return fail(J3D_EUNSUPPORTED, "use_graph with ranks sharing a GPU: graph launches of one CUDA context share "
+                                          "its internal streams, so one rank's captured epoch wait can block the "
+                                          "peer work it waits for");
         c->persist_grid = std::max(1, c->grid_cap / std::max(1, c->co_resident));
         if (c->host_needed && !c->host_connected) host_connect(c);
         if (c->ctl_needed && !c->ctl_connected) ctl_connect(c);

@@ -27,6 +27,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <fcntl.h>
 #include <sys/mman.h>
@@ -50,6 +51,16 @@
 #include "plan.h"
 
 namespace j3d {
+
+// NVTX range on the host timeline around each phase the library enqueues
+// (stencil, pack, exchange, unpack, waits): header-only NVTX v3, a no-op unless
+// a profiler is attached (phase ranges for the exposed-halo cross-check)
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx&) = delete;
+    Nvtx& operator=(const Nvtx&) = delete;
+};
 
 struct Error : std::runtime_error {
     int code;
@@ -171,6 +182,8 @@ struct jacobi3d {
     size_t shm_bytes = 0;
     std::vector<char*> shm_base;      // mapped segments (index = rank; own included)
     std::vector<char*> shm_dev;       // device-visible address of each mapped segment
+    CopyDesc* d_stage_out = nullptr;  // [(q*nl + l)*6 + f] send buffer -> own segment (staged D2H)
+    CopyDesc* d_stage_in = nullptr;   // [(q*nl + l)*6 + f] neighbour's segment -> receive buffer (staged H2D)
 
     // device tables
     StencilDesc* d_descs = nullptr;

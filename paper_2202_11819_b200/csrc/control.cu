@@ -58,6 +58,7 @@ char* map_segment(const std::string& nm, bool create) {
 
 // publish seq = k, then wait until every rank reached k
 void arrive_and_wait(jacobi3d* c, uint64_t k) {
+    Nvtx nv("j3d.collective");
     __atomic_store_n(&seg(c, c->rank)->seq, k, __ATOMIC_RELEASE);
     const double limit = timeout_s();
     const auto t0 = std::chrono::steady_clock::now();

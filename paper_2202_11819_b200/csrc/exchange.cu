@@ -106,6 +106,30 @@ void host_connect(jacobi3d* c) {  // map every neighbour rank's segment
         c->shm_dev[r] = (char*)d;
     }
     c->host_connected = true;
+    // copy tables of the staged exchange [(q*nl + l)*6 + f]: device send buffer ->
+    // this rank's segment (D2H), the neighbour's segment -> device receive buffer
+    // (H2D), both through the segments' device-mapped addresses
+    const int nl = c->n_local;
+    std::vector<CopyDesc> out((size_t)2 * nl * 6), in((size_t)2 * nl * 6);
+    std::memset(out.data(), 0, out.size() * sizeof(CopyDesc));
+    std::memset(in.data(), 0, in.size() * sizeof(CopyDesc));
+    for (int q = 0; q < 2; ++q)
+        for (int l = 0; l < nl; ++l)
+            for (int f = 0; f < 6; ++f) {
+                if (c->kind[l][f] != PEER_HOST) continue;
+                const size_t i = ((size_t)q * nl + l) * 6 + f;
+                const int r = c->plan.blocks[c->plan.blocks[c->gid[l]].nbr[f]].owner;
+                out[i].src = c->contiguous(c->face_buf(l, f, q, false), f);
+                out[i].dst = c->contiguous((double*)(c->shm_dev[c->rank] + shm_area_offset(c, l, f, q)), f);
+                in[i].src = c->contiguous((double*)(c->shm_dev[r] + shm_area_offset(c, c->nbr_local[l][f], f ^ 1, q)), f);
+                in[i].dst = c->contiguous(c->face_buf(l, f, q, true), f);
+                out[i].na = in[i].na = (int32_t)c->face_na(f);
+                out[i].nb = in[i].nb = (int32_t)c->face_nb(f);
+            }
+    if (!c->d_stage_out) CK(cudaMalloc(&c->d_stage_out, out.size() * sizeof(CopyDesc)));
+    if (!c->d_stage_in) CK(cudaMalloc(&c->d_stage_in, in.size() * sizeof(CopyDesc)));
+    CK(cudaMemcpy(c->d_stage_out, out.data(), out.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_stage_in, in.data(), in.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
 }
 
 void host_teardown(jacobi3d* c) {
@@ -122,15 +146,18 @@ void host_teardown(jacobi3d* c) {
 // D2H of my send buffers into my segment, epoch signal into each neighbour's
 // segment flags, wait for theirs, H2D of their staging areas into my receive
 // buffers.  Flags: toggle protocol on slot (same rules as P2P, see p2p_sync).
+// The D2H / H2D moves are copy kernels over the segments' device-mapped
+// addresses (zero-copy through pinned host memory; write-through stores,
+// cache-volatile loads), not DMA engine copies: the copy engines are shared
+// by every stream of a CUDA context, so with ranks that are threads of one
+// process a copy waiting for a peer's flag could sit in front of the peer's
+// own D2H copy in an engine queue (a deadlock seen on the GPU).
 void host_exchange(jacobi3d* c, int par, int slot, cudaStream_t st) {
     if (!c->host_needed) return;
     const int n = c->n_gpus;
-    for (int l = 0; l < c->n_local; ++l)
-        for (int f = 0; f < 6; ++f)
-            if (c->kind[l][f] == PEER_HOST)
-                CK(cudaMemcpyAsync(c->shm_base[c->rank] + shm_area_offset(c, l, f, par),
-                                   c->face_buf(l, f, par, false), (size_t)face_cells(c->plan.ext, f) * 8,
-                                   cudaMemcpyDeviceToHost, st));
+    const int64_t mx = std::max(face_cells(c->plan.ext, 0), std::max(face_cells(c->plan.ext, 2), face_cells(c->plan.ext, 4)));
+    CK(launch_stage_copy(c->d_stage_out + (int64_t)par * c->n_local * 6, 6, c->n_local, mx, false, st));
+    count_launch(c, -1);
     for (int r : c->peer_ranks)
         DK(g_drv.write64((CUstream)st, (CUdeviceptr)((uint64_t*)c->shm_dev[r] + slot * n + c->rank), 1, 0));
     for (int r : c->peer_ranks) {
@@ -138,14 +165,8 @@ void host_exchange(jacobi3d* c, int par, int slot, cudaStream_t st) {
         DK(g_drv.wait64((CUstream)st, f, 1, CU_STREAM_WAIT_VALUE_EQ));
         DK(g_drv.write64((CUstream)st, f, 0, 0));
     }
-    for (int l = 0; l < c->n_local; ++l)
-        for (int f = 0; f < 6; ++f)
-            if (c->kind[l][f] == PEER_HOST) {
-                const int r = c->plan.blocks[c->plan.blocks[c->gid[l]].nbr[f]].owner;
-                CK(cudaMemcpyAsync(c->face_buf(l, f, par, true),
-                                   c->shm_base[r] + shm_area_offset(c, c->nbr_local[l][f], f ^ 1, par),
-                                   (size_t)face_cells(c->plan.ext, f) * 8, cudaMemcpyHostToDevice, st));
-            }
+    CK(launch_stage_copy(c->d_stage_in + (int64_t)par * c->n_local * 6, 6, c->n_local, mx, true, st));
+    count_launch(c, -1);
 }
 
 // epoch barrier through the host segments (refresh pre-barrier of the host backend)
@@ -163,6 +184,7 @@ void host_sync(jacobi3d* c, int slot, cudaStream_t st) {
 
 void cross_gpu_exchange(jacobi3d* c, int par, int slot, cudaStream_t st) {
     if (c->n_gpus == 1 || c->skip_exchange) return;
+    Nvtx nv("j3d.exchange");
     nccl_exchange(c, par, st);
     p2p_sync(c, slot, st);
     host_exchange(c, par, slot, st);

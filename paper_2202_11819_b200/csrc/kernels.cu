@@ -509,6 +509,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
         const uint32_t touch = (x0 == 0 ? 1u : 0u) | (x0 + T::TX >= nx ? 2u : 0u) | (y0 == 0 ? 4u : 0u) |
                                (y0 + T::TY >= ny ? 8u : 0u);
         const bool whole = x0 + T::TX <= nx && y0 + T::TY <= ny;  // no cell of the tile is outside the block
+        const bool fullw = T::MAP == 1 && whole && x0 == 0 && nx == T::TX;  // compute_plane_s FULL
         // x-face destinations of this tile: wide tiles load them once per item
         // (registers are plentiful there), narrow 2-CTA/SM tiles per plane
         constexpr bool HOISTX = T::TX >= 128;
@@ -734,15 +735,22 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
         };
 
         // MAP 1: the same plane update with one cell per lane and column step 32
-        auto compute_plane_s = [&](auto mode_tag, auto whole_tag, int z, uint32_t fm, const double* pm,
-                                   const double* pc, const double* pp) {
+        // FULL: the tile spans the block's whole width (x0 == 0, nx == TX; e.g.
+        // the 96^3 blocks of BASELINE configs[4]) and is whole: the x-edge cells
+        // are lane 0 of k = 0 and lane 31 of k = KPL-1 at compile time, so the
+        // x-neighbour offsets, the +x capture and the store predicates are
+        // per-row constants instead of per-cell selects
+        auto compute_plane_s = [&](auto mode_tag, auto whole_tag, auto full_tag, int z, uint32_t fm,
+                                   const double* pm, const double* pc, const double* pp) {
             constexpr int MODE = decltype(mode_tag)::value;
-            constexpr bool WHOLE = decltype(whole_tag)::value;
+            constexpr bool FULL = decltype(full_tag)::value;
+            constexpr bool WHOLE = decltype(whole_tag)::value || FULL;
             constexpr int KPL = T::KPL;
             double* op = obase + (int64_t)(z + 1) * zs;
             double cap0[RPW], cap1[RPW];
             const int xlast = nx - 1 - x0;
-            const int klast = xlast >> 5, lane_last = xlast & 31;
+            const int klast = FULL ? KPL - 1 : xlast >> 5, lane_last = FULL ? 31 : xlast & 31;
+            const int kedge_ = FULL ? KPL - 1 : kedge;
             double* zdst = nullptr;
             int64_t zsb = 0;
             double* ymd = nullptr;
@@ -775,7 +783,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                     // block x edge: the neighbour outside the block comes from the
                     // stage's x ghost vector (offsets fixed for the item)
                     const int om = (k == 0 && xlf) ? xlb + r * (1 - W) : -1;
-                    const int oq = (k == kedge && xrf) ? xrb + r * (1 - W) : 1;
+                    const int oq = (k == kedge_ && xrf) ? xrb + r * (1 - W) : 1;
                     const double sv = sum7(p[0], p[om], p[oq], p[-W], p[W], pm[off], pp[off]);
                     const double v = div7_fast(sv);
                     rare |= div7_rare(v);
@@ -803,7 +811,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                     double* q = F.p + (int64_t)z * F.sb;
 #pragma unroll
                     for (int r = 0; r < RPW; ++r)
-                        if (yl + r < ny) {
+                        if (WHOLE || yl + r < ny) {
                             q[(int64_t)(yl + r) * F.sa] = cap0[r];
                         }
                 }
@@ -812,7 +820,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                     double* q = F.p + (int64_t)z * F.sb;
 #pragma unroll
                     for (int r = 0; r < RPW; ++r)
-                        if (yl + r < ny) {
+                        if (WHOLE || yl + r < ny) {
                             q[(int64_t)(yl + r) * F.sa] = cap1[r];
                         }
                 }
@@ -827,7 +835,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                         const int off = r * W + 32 * k;
                         const double* p = pc + off;
                         const int om = (k == 0 && xlf) ? xlb + r * (1 - W) : -1;
-                        const int oq = (k == kedge && xrf) ? xrb + r * (1 - W) : 1;
+                        const int oq = (k == kedge_ && xrf) ? xrb + r * (1 - W) : 1;
                         const double v = div7(sum7(p[0], p[om], p[oq], p[-W], p[W], pm[off], pp[off]));
                         op[r * pitch + 32 * k] = v;
                         const uint32_t m = rare ? fm : (rare_faces & fm);
@@ -857,10 +865,18 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
             using M1 = std::integral_constant<int, 1>;
             using M2 = std::integral_constant<int, 2>;
             if constexpr (T::MAP == 1) {
-                if (fm & ~3u) compute_plane_s(M2{}, std::false_type{}, z, fm, pm, pc, pp);
-                else if (fm) compute_plane_s(M1{}, std::false_type{}, z, fm, pm, pc, pp);
-                else if (whole) compute_plane_s(M0{}, std::true_type{}, z, 0u, pm, pc, pp);
-                else compute_plane_s(M0{}, std::false_type{}, z, 0u, pm, pc, pp);
+                using F_ = std::false_type;
+                using T_ = std::true_type;
+                if (fullw) {
+                    if (fm & ~3u) compute_plane_s(M2{}, T_{}, T_{}, z, fm, pm, pc, pp);
+                    else if (fm) compute_plane_s(M1{}, T_{}, T_{}, z, fm, pm, pc, pp);
+                    else compute_plane_s(M0{}, T_{}, T_{}, z, 0u, pm, pc, pp);
+                } else {
+                    if (fm & ~3u) compute_plane_s(M2{}, F_{}, F_{}, z, fm, pm, pc, pp);
+                    else if (fm) compute_plane_s(M1{}, F_{}, F_{}, z, fm, pm, pc, pp);
+                    else if (whole) compute_plane_s(M0{}, T_{}, F_{}, z, 0u, pm, pc, pp);
+                    else compute_plane_s(M0{}, F_{}, F_{}, z, 0u, pm, pc, pp);
+                }
             } else {
                 if (fm & ~3u) compute_plane(M2{}, std::false_type{}, z, fm, pm, pc, pp);
                 else if (fm) compute_plane(M1{}, std::false_type{}, z, fm, pm, pc, pp);
@@ -912,6 +928,33 @@ __global__ void __launch_bounds__(256) copy_faces_kernel(const CopyDesc* __restr
             const int64_t b = idx / na, a = idx - b * na;
             const FaceRef src = g[k].src, dst = g[k].dst;
             dst.p[a * dst.sa + b * dst.sb] = src.p[a * src.sa + b * src.sb];
+        }
+    }
+}
+
+// Host-staged exchange moves (exchange.cu host_exchange): the same strided
+// copy, one side in pinned host memory mapped into the device.  To host:
+// write-through stores (st.global.wt: straight to system memory); from host:
+// cache-volatile loads (ld.global.cv: never a line cached from an earlier
+// epoch of the staging area).
+__global__ void __launch_bounds__(256) stage_copy_kernel(const CopyDesc* __restrict__ descs, int per_group,
+                                                         int from_host) {
+    const CopyDesc* g = descs + (int64_t)blockIdx.y * per_group;
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int k = 0; k < per_group; ++k) {
+        const int64_t na = g[k].na, nb = g[k].nb;
+        if (idx < na * nb) {
+            const int64_t b = idx / na, a = idx - b * na;
+            const double* sp = g[k].src.p + a * g[k].src.sa + b * g[k].src.sb;
+            double* dp = g[k].dst.p + a * g[k].dst.sa + b * g[k].dst.sb;
+            double v;
+            if (from_host) {
+                asm volatile("ld.global.cv.f64 %0, [%1];" : "=d"(v) : "l"(sp) : "memory");
+                *dp = v;
+            } else {
+                v = *sp;
+                asm volatile("st.global.wt.f64 [%0], %1;" ::"l"(dp), "d"(v) : "memory");
+            }
         }
     }
 }
@@ -1174,7 +1217,8 @@ cudaError_t preload_kernels(int kind) {
     }
     if (e != cudaSuccess) return e;
     cudaFuncAttributes a;
-    const void* fns[] = {(const void*)wait_counters_kernel, (const void*)copy_faces_kernel, (const void*)init_kernel,
+    const void* fns[] = {(const void*)wait_counters_kernel, (const void*)copy_faces_kernel,
+                         (const void*)stage_copy_kernel, (const void*)init_kernel,
                          (const void*)checksum_kernel, (const void*)residual_kernel};
     for (const void* f : fns)
         if ((e = cudaFuncGetAttributes(&a, f)) != cudaSuccess) return e;
@@ -1206,6 +1250,15 @@ cudaError_t launch_copy_faces(const CopyDesc* d, int per_group, int groups, int6
     const int64_t nblk = (max_cells + 255) / 256;
     if (nblk > 0x7fffffff || groups > 65535) return cudaErrorInvalidValue;
     copy_faces_kernel<<<dim3((unsigned)nblk, (unsigned)groups), 256, 0, st>>>(d, per_group);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stage_copy(const CopyDesc* d, int per_group, int groups, int64_t max_cells, bool from_host,
+                              cudaStream_t st) {
+    if (groups <= 0 || max_cells <= 0) return cudaSuccess;
+    const int64_t nblk = (max_cells + 255) / 256;
+    if (nblk > 0x7fffffff || groups > 65535) return cudaErrorInvalidValue;
+    stage_copy_kernel<<<dim3((unsigned)nblk, (unsigned)groups), 256, 0, st>>>(d, per_group, from_host ? 1 : 0);
     return cudaGetLastError();
 }
 

@@ -42,6 +42,8 @@ cudaError_t launch_div7_selftest(uint64_t n, uint64_t seed, unsigned long long* 
                                  cudaStream_t st);
 cudaError_t launch_wait_counters(const unsigned int* const* ptrs, int n, uint32_t need, uint64_t limit_ns,
                                  cudaStream_t st);
+cudaError_t launch_stage_copy(const CopyDesc* d, int per_group, int groups, int64_t max_cells, bool from_host,
+                              cudaStream_t st);
 cudaError_t launch_copy_faces(const CopyDesc* d, int per_group, int groups, int64_t max_cells, cudaStream_t st);
 cudaError_t launch_init(const BlockGeom* g, int nblocks, int max_nx, int64_t max_rows, int kind, const double* p,
                         uint64_t seed, double boundary, int64_t gx, int64_t gy, int64_t gz, cudaStream_t st);

@@ -34,6 +34,7 @@ static uint64_t wait_limit_ns() { return (uint64_t)(timeout_s() * 1e9); }
 
 void stencil(jacobi3d* c, int begin, int count, int parity, cudaStream_t st, int l) {
     if (count <= 0) return;
+    Nvtx nv("j3d.stencil");
     StencilLaunch L;
     L.descs = c->d_descs;
     L.tmaps = c->d_tmaps;
@@ -76,6 +77,9 @@ void stencil(jacobi3d* c, int begin, int count, int parity, cudaStream_t st, int
 
 void copies(jacobi3d* c, CopyDesc* table, int parity, int l, int face, bool fused, cudaStream_t st) {
     // table layout [(q*nl + l)*6 + f]
+    const bool unpack = table == c->d_unpack || table == c->d_unpack_nccl || table == c->d_unpack_peer ||
+                        table == c->d_unpack_local;
+    Nvtx nv(unpack ? "j3d.unpack" : table == c->d_push ? "j3d.push" : "j3d.pack");
     const int nl = c->n_local;
     if (l < 0) {  // batched: every local block, fused over faces
         int64_t mx = 0;
@@ -104,6 +108,7 @@ void copies(jacobi3d* c, CopyDesc* table, int parity, int l, int face, bool fuse
 // every earlier use of them (the caller's state change, e.g. init or
 // set_block, or the last iteration of a previous run).
 void refresh(jacobi3d* c, int par) {
+    Nvtx nv("j3d.refresh");
     const int rc = (int)(c->refresh_count & 1);
     c->refresh_count++;
     if (c->n_gpus > 1) {
@@ -266,6 +271,7 @@ void drop_graphs(jacobi3d* c) {
 
 void do_iterate(jacobi3d* c, int64_t n) {
     if (n <= 0) return;
+    Nvtx nv("j3d.iterate");
     if (c->halos_stale) {
         if (c->n_gpus > 1)
             throw Error(J3D_ESTATE, "halos are stale after set_block: call jacobi3d_refresh_halos on every rank");
@@ -367,6 +373,8 @@ void destroy_ctx(jacobi3d* c) {
     cudaFree(c->d_pack);
     cudaFree(c->d_unpack);
     cudaFree(c->d_unpack_nccl);
+    cudaFree(c->d_stage_out);
+    cudaFree(c->d_stage_in);
     cudaFree(c->d_push);
     cudaFree(c->d_item_slab);
     cudaFree(c->d_slab_deps);
@@ -393,6 +401,7 @@ double timeout_s() {
 }
 
 void wait_stream(jacobi3d* c, cudaStream_t st) {
+    Nvtx nv("j3d.wait");
     if (c->n_gpus == 1) {
         CK(cudaStreamSynchronize(st));
         return;

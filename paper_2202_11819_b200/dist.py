@@ -89,11 +89,19 @@ class ThreadGroup:
         try:
             self._recs[rank] = ctx.ipc_export()
             self._bar.wait(timeout=600)
-            ctx.ipc_connect(list(self._recs))
-            self._bar.wait(timeout=600)
         except BaseException:
             self._bar.abort()
+            ctx.close()
             raise
+        err = None
+        try:  # a refused connect (the same answer on every rank) still meets the others below
+            ctx.ipc_connect(list(self._recs))
+        except Exception as e:  # noqa: BLE001
+            err = e
+        self._bar.wait(timeout=600)
+        if err is not None:
+            ctx.close()
+            raise err
         return ctx
 
     def barrier(self):
