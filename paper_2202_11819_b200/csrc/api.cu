@@ -332,6 +332,30 @@ int jacobi3d_ipc_connect(jacobi3d_t* c, const uint8_t* all, size_t len_per_rank)
                                           "its internal streams, so one rank's captured epoch wait can block the "
                                           "peer work it waits for");
         c->persist_grid = std::max(1, c->grid_cap / std::max(1, c->co_resident));
+        if (c->co_resident > 1) {
+            // ranks sharing this GPU: every stream at the default priority.  High-priority
+            // streams of one context share few hardware queues, so one rank's epoch wait on
+            // its overlap exchange stream could sit in front of the peer's signal (seen as
+            // intermittent hangs of the overlap mode with 2 and 4 thread ranks); no work has
+            // been queued on these streams yet
+            // ranks sharing this GPU: ONE stream per rank.  The per-block streams and the
+            // overlap mode's exchange stream become the main stream (same launches in the
+            // same order, no concurrency inside a rank): with several streams per rank,
+            // one of which waits on peers' flags, runs deadlocked intermittently (overlap:
+            // 1 in ~10-40 runs at 2 and 4 thread ranks; per-block: 1 in ~4 suites) -- a
+            // hardware queue shared with a peer's stream; no work has been queued on
+            // these streams yet
+            for (auto* v : {&c->lo, &c->hi})
+                for (auto& st : *v) {
+                    CK(cudaStreamDestroy(st));
+                    st = c->main;
+                }
+            c->streams_aliased = true;
+            if (c->xstream) {
+                CK(cudaStreamDestroy(c->xstream));
+                c->xstream = nullptr;
+            }
+        }
         if (c->host_needed && !c->host_connected) host_connect(c);
         if (c->ctl_needed && !c->ctl_connected) ctl_connect(c);
         if (c->p2p_needed && !c->p2p_connected) {

@@ -172,6 +172,7 @@ struct jacobi3d {
     uint64_t ctl_seq = 0;
     std::vector<char*> ctl_base;   // mapped segments (index = rank; own included)
     int co_resident = 1;           // ranks of this job on this GPU (threads of one process)
+    bool streams_aliased = false;  // co_resident > 1: lo / hi are the main stream (api.cu connect)
     int persist_grid = 0;          // persistent grid: grid_cap / co_resident (all co-resident ranks fit)
     uint64_t* host_scratch = nullptr;  // pinned: residual / checksum results
     // host staging (J3D_XCHG_HOST): one POSIX shared-memory segment per rank,

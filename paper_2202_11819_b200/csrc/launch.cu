@@ -150,15 +150,17 @@ void enqueue_iteration(jacobi3d* c, int p, bool first, bool last) {
             // exterior items (those touching a peer face) first; the exchange
             // of their faces runs on `comm` while the interior items update
             // (Fig 1 manual overlap, L79-107; ODF-driven overlap, L146-156)
+            // (ranks sharing a GPU: no exchange stream, the exchange runs on main; api.cu)
+            cudaStream_t xs = c->xstream ? c->xstream : c->main;
             stencil(c, 0, c->n_ext, p, c->main, -1);
             CK(cudaEventRecord(c->ev_ext[q], c->main));
-            CK(cudaStreamWaitEvent(c->xstream, c->ev_ext[q], 0));
-            if (unf) copies(c, c->d_pack_peer, q, -1, 0, true, c->xstream);
-            else if (c->direct_push) copies(c, c->d_push, q, -1, 0, true, c->xstream);
-            cross_gpu_exchange(c, q, q, c->xstream);
-            if (unf) copies(c, c->d_unpack_peer, q, -1, 0, true, c->xstream);
-            else if (c->direct_nccl_unpack) copies(c, c->d_unpack_nccl, q, -1, 0, true, c->xstream);
-            CK(cudaEventRecord(c->ev_comm[q], c->xstream));
+            CK(cudaStreamWaitEvent(xs, c->ev_ext[q], 0));
+            if (unf) copies(c, c->d_pack_peer, q, -1, 0, true, xs);
+            else if (c->direct_push) copies(c, c->d_push, q, -1, 0, true, xs);
+            cross_gpu_exchange(c, q, q, xs);
+            if (unf) copies(c, c->d_unpack_peer, q, -1, 0, true, xs);
+            else if (c->direct_nccl_unpack) copies(c, c->d_unpack_nccl, q, -1, 0, true, xs);
+            CK(cudaEventRecord(c->ev_comm[q], xs));
             stencil(c, c->n_ext, c->n_items - c->n_ext, p, c->main, -1);
             if (unf) {
                 copies(c, c->d_pack_local, q, -1, 0, true, c->main);
@@ -321,11 +323,19 @@ void do_iterate(jacobi3d* c, int64_t n) {
 
 void destroy_ctx(jacobi3d* c) {
     if (!c) return;
+    // J3D_TRACE_DESTROY=1: print each step (diagnosing teardown of thread ranks)
+    static const bool trace = std::getenv("J3D_TRACE_DESTROY") != nullptr;
+    auto step = [&](const char* what) {
+        if (trace) std::fprintf(stderr, "[j3d destroy rank %d] %s\n", c->rank, what), std::fflush(stderr);
+    };
     cudaSetDevice(c->device);
+    step("sync");
     try {
         sync_streams(c);
     } catch (...) {
+        step("sync timed out");
     }
+    step("barrier");
     // collective (jacobi3d.h): once every rank is here no peer still touches this
     // rank's arena -- persistent launches read the peers' slab counters over NVLink
     // until their own last iteration -- so freeing it cannot fault a slower peer
@@ -337,6 +347,7 @@ void destroy_ctx(jacobi3d* c) {
             abort_comm = true;
         }
     }
+    step("graphs/events/streams");
     drop_graphs(c);
     for (auto& pr : c->prof_events) {
         cudaEventDestroy(pr.first);
@@ -353,17 +364,22 @@ void destroy_ctx(jacobi3d* c) {
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_t0) cudaEventDestroy(c->ev_t0);
     if (c->ev_t1) cudaEventDestroy(c->ev_t1);
-    for (auto s : c->lo) if (s) cudaStreamDestroy(s);
-    for (auto s : c->hi) if (s) cudaStreamDestroy(s);
+    if (!c->streams_aliased) {
+        for (auto s : c->lo) if (s) cudaStreamDestroy(s);
+        for (auto s : c->hi) if (s) cudaStreamDestroy(s);
+    }
     if (c->comm) {
         if (abort_comm) ncclCommAbort(c->comm);
         else ncclCommDestroy(c->comm);
     }
+    step("ipc/host/ctl");
     for (size_t r = 0; r < c->peer_base.size(); ++r)
         if (c->peer_base[r] && r < c->peer_ipc.size() && c->peer_ipc[r]) cudaIpcCloseMemHandle(c->peer_base[r]);
     host_teardown(c);
     ctl_teardown(c);
+    step("free host scratch");
     if (c->host_scratch) cudaFreeHost(c->host_scratch);
+    step("free device");
     if (c->main) cudaStreamDestroy(c->main);
     cudaFree(c->d_descs);
     cudaFree(c->d_tmaps);
@@ -387,6 +403,7 @@ void destroy_ctx(jacobi3d* c) {
     cudaFree(c->d_geom);
     cudaFree(c->d_sched);
     cudaFree(c->arena);
+    step("done");
     delete c;
 }
 
@@ -434,8 +451,8 @@ void wait_stream(jacobi3d* c, cudaStream_t st) {
 // rank's next call (a deadlock).
 void sync_streams(jacobi3d* c) {
     if (c->main) wait_stream(c, c->main);
-    for (auto s : c->lo) if (s) wait_stream(c, s);
-    for (auto s : c->hi) if (s) wait_stream(c, s);
+    for (auto s : c->lo) if (s && s != c->main) wait_stream(c, s);
+    for (auto s : c->hi) if (s && s != c->main) wait_stream(c, s);
     if (c->xstream) wait_stream(c, c->xstream);
 }
 
