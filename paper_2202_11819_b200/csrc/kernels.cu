@@ -99,16 +99,23 @@ __device__ __forceinline__ void wait_counter(const unsigned int* p, uint32_t nee
     }
 }
 
-__device__ __noinline__ void wait_slabs(const IterCtl ctl, int it, uint32_t iters) {
+// Called by the whole producer warp: lane j polls the item's j-th dependency
+// (one round trip for all of them instead of up to MAX_DEPS in sequence), then
+// lane 0 -- which issues the TMA loads -- orders them after every lane's
+// acquire (the warp barrier, a fence at the acquires' scope) and after the
+// generic-proxy writes they observed (proxy fence).
+__device__ __noinline__ void wait_slabs(const IterCtl ctl, int it, uint32_t iters, int lane) {
     const uint32_t need = iters * ctl.target;
     const unsigned int* const* dp = ctl.slab_deps + (int64_t)(ctl.item_slab[it] & SLAB_MASK) * MAX_DEPS;
-    for (int j = 0; j < MAX_DEPS; ++j) {
-        const uintptr_t p = reinterpret_cast<uintptr_t>(dp[j]);
-        if (!p) break;
-        // bit 0 tags a peer GPU's counter: acquire at system scope
-        wait_counter(reinterpret_cast<const unsigned int*>(p & ~uintptr_t(1)), need, (p & 1) != 0, ctl.timeout_ns);
+    const uintptr_t p = lane < MAX_DEPS ? reinterpret_cast<uintptr_t>(dp[lane]) : 0;
+    // bit 0 tags a peer GPU's counter: acquire at system scope
+    if (p) wait_counter(reinterpret_cast<const unsigned int*>(p & ~uintptr_t(1)), need, (p & 1) != 0, ctl.timeout_ns);
+    __syncwarp();
+    if (lane == 0) {
+        if (ctl.sys) __threadfence_system();
+        else __threadfence();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
     }
-    asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 __device__ __forceinline__ void tmap_acquire(const CUtensorMap* m) {
@@ -398,27 +405,38 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
     __syncthreads();
 
     if (warp == NCW) {  // ---------------- producer warp: item scheduling + TMA plane loads
-        if (lane == 0) {
-            int s = 0, qs = 0;
-            uint32_t ph = 0, qph = 0;
-            const int tma_mode = (flags >> 2) & 3;
-            uint64_t pol_first = 0, pol_last = 0;
-            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
-            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
-            const int total = n_items * ctl.n_iter;
-            for (;;) {
-                int g = (int)atomicAdd(&sched[0], 1u);
-                if (g >= total) g = -1;
+        int s = 0, qs = 0;
+        uint32_t ph = 0, qph = 0;
+        const int tma_mode = (flags >> 2) & 3;
+        const int total = n_items * ctl.n_iter;
+        // lane 0 claims items and issues every TMA load; the whole warp polls the
+        // persistent launch's dependency counters.  The next item is claimed when
+        // the current one starts, so the claim's round trip overlaps its planes.
+        int g = 0;
+        if (lane == 0) g = (int)atomicAdd(&sched[0], 1u);
+        g = __shfl_sync(0xffffffffu, g, 0);
+        for (;;) {
+            if (g >= total) g = -1;
+            int gn = 0;
+            if (lane == 0) {
+                if (g >= 0) gn = (int)atomicAdd(&sched[0], 1u);
                 mbar_wait(&qempty[qs], qph ^ 1);
                 queue[qs] = g;
                 mbar_arrive(&qfull[qs]);
-                if (++qs == IQ) { qs = 0; qph ^= 1; }
-                if (g < 0) break;
-                const int k = g / n_items, it = g - k * n_items;
+            }
+            if (++qs == IQ) { qs = 0; qph ^= 1; }
+            if (g < 0) break;
+            const int k = g / n_items, it = g - k * n_items;
+            // iteration 0 of a call waits only for peers (this GPU's previous
+            // launch is complete in stream order)
+            if (ctl.done && (k > 0 || ctl.sys)) wait_slabs(ctl, it, ctl.base + (uint32_t)k, lane);
+            if (lane == 0) {
+                uint64_t pol_first = 0, pol_last = 0;
+                if (tma_mode) {
+                    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+                    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
+                }
                 const WorkItem w = items[it];
-                // iteration 0 of a call waits only for peers (this GPU's previous
-                // launch is complete in stream order)
-                if (ctl.done && (k > 0 || ctl.sys)) wait_slabs(ctl, it, ctl.base + (uint32_t)k);
                 const int bp = 2 * w.blk + (parity ^ (k & 1));
                 const CUtensorMap* tm = tmaps + bp;
                 const CUtensorMap* tx = tmapsx + bp;
@@ -470,6 +488,9 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                     if (++s == NSTAGE) { s = 0; ph ^= 1; }
                 }
             }
+            g = __shfl_sync(0xffffffffu, gn, 0);
+        }
+        if (lane == 0) {
             __threadfence();
             if (atomicAdd(&sched[1], 1u) == gridDim.x - 1) {  // every CTA has taken its last item
                 sched[0] = 0;
@@ -520,6 +541,24 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
             if constexpr (HOISTX) return f == 0 ? fxm : fxp;
             else return load_face(&d->epi[f]);
         };
+        // one-cell map with 4+ rows per warp (register room): the x-face stores'
+        // destinations once per item in compact form -- this warp's first row at
+        // z = 0 and the plane stride (x faces are contiguous in y: sa == 1,
+        // setup.cu checks) -- instead of three descriptor loads per plane
+        constexpr bool HOISTX1 = T::MAP == 1 && RPW >= 4;
+        double* xq0 = nullptr;
+        double* xq1 = nullptr;
+        int32_t xsb0 = 0, xsb1 = 0;
+        if (HOISTX1 && (epi & touch & 1u)) {
+            const FaceRef F = load_face(&d->epi[0]);
+            xq0 = F.p + yl;
+            xsb0 = (int32_t)F.sb;
+        }
+        if (HOISTX1 && (epi & touch & 2u)) {
+            const FaceRef F = load_face(&d->epi[1]);
+            xq1 = F.p + yl;
+            xsb1 = (int32_t)F.sb;
+        }
         const int sbase = (warp * RPW + 1) * W + (T::MAP == 1 ? lane : 2 * lane) + T::HX;  // smem offset of the first cell
 
         // wait for the stage of plane zz, patch its ghosts (fused prologue) if needed
@@ -807,22 +846,36 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
             }
             if constexpr (MODE >= 1) {  // x faces: the lane owning x = 0 / x = nx-1
                 if ((fm & 1u) && x0 == 0 && lane == 0) {
-                    const FaceRef F = face_x(0);
-                    double* q = F.p + (int64_t)z * F.sb;
+                    if constexpr (HOISTX1) {
+                        double* q = xq0 + (int64_t)z * xsb0;
 #pragma unroll
-                    for (int r = 0; r < RPW; ++r)
-                        if (WHOLE || yl + r < ny) {
-                            q[(int64_t)(yl + r) * F.sa] = cap0[r];
-                        }
+                        for (int r = 0; r < RPW; ++r)
+                            if (WHOLE || yl + r < ny) q[r] = cap0[r];
+                    } else {
+                        const FaceRef F = face_x(0);
+                        double* q = F.p + (int64_t)z * F.sb;
+#pragma unroll
+                        for (int r = 0; r < RPW; ++r)
+                            if (WHOLE || yl + r < ny) {
+                                q[(int64_t)(yl + r) * F.sa] = cap0[r];
+                            }
+                    }
                 }
                 if ((fm & 2u) && klast < KPL && lane == lane_last) {
-                    const FaceRef F = face_x(1);
-                    double* q = F.p + (int64_t)z * F.sb;
+                    if constexpr (HOISTX1) {
+                        double* q = xq1 + (int64_t)z * xsb1;
 #pragma unroll
-                    for (int r = 0; r < RPW; ++r)
-                        if (WHOLE || yl + r < ny) {
-                            q[(int64_t)(yl + r) * F.sa] = cap1[r];
-                        }
+                        for (int r = 0; r < RPW; ++r)
+                            if (WHOLE || yl + r < ny) q[r] = cap1[r];
+                    } else {
+                        const FaceRef F = face_x(1);
+                        double* q = F.p + (int64_t)z * F.sb;
+#pragma unroll
+                        for (int r = 0; r < RPW; ++r)
+                            if (WHOLE || yl + r < ny) {
+                                q[(int64_t)(yl + r) * F.sa] = cap1[r];
+                            }
+                    }
                 }
             }
             if (rare || rare_faces) {
@@ -1128,7 +1181,13 @@ cudaError_t launch_div7_selftest(uint64_t n, uint64_t seed, unsigned long long* 
     X(18, -96, 6, 2, 8, 2)  /* 96x12 (RPW 2)                             */ \
     X(19, -96, 8, 2, 7, 2)  /* 96x16, 7 stages, 2 CTAs/SM                */ \
     X(20, 192, 8, 2, 5, 1)  /* 192x16, 5 x 29 KB stages                  */ \
-    X(21, 192, 12, 2, 5, 1) /* 192x24, 5 stages                          */
+    X(21, 192, 12, 2, 5, 1) /* 192x24, 5 stages                          */ \
+    X(22, -96, 4, 4, 6, 2)  /* 96x16 one cell per lane, 4 rows per warp  */ \
+    X(23, -96, 4, 4, 7, 2)  /* 96x16, RPW 4, 7 stages                    */ \
+    X(24, -96, 4, 6, 5, 2)  /* 96x24, RPW 6                              */ \
+    X(25, -96, 4, 4, 4, 3)  /* 96x16, RPW 4, 3 CTAs/SM                   */ \
+    X(26, 192, 6, 4, 5, 1)  /* 192x24, 4 rows per warp                   */ \
+    X(27, 192, 8, 3, 5, 1)  /* 192x24, 3 rows per warp                   */
 
 template <class T>
 static cudaError_t launch_t(const StencilLaunch& L, cudaStream_t st) {
@@ -1161,7 +1220,7 @@ static cudaError_t occ_t(int* blocks) {
 
 #define J3D_TYPE(k, tx, ncw, rpw, ns, mb) Tile<(tx > 0 ? tx : -tx), ncw, rpw, ns, mb, (tx > 0 ? 0 : 1)>
 
-int num_tile_kinds() { return 22; }
+int num_tile_kinds() { return 28; }
 
 TileShape tile_shape(int kind) {
     switch (kind) {

@@ -181,6 +181,9 @@ void build_tables(jacobi3d* c) {
                         }
                     }
                 }
+                for (int f = 0; f < 2; ++f)  // x-face destinations are contiguous in y (kernels.cu HOISTX1)
+                    if ((d.epi_mask & (1u << f)) && d.epi[f].sa != 1)
+                        throw Error(J3D_EUNSUPPORTED, "x-face destination with a row stride != 1");
                 if (d.epi_mask | d.pro_mask | d.pro_tma) c->faces_fused = true;
             }
         }
@@ -362,7 +365,11 @@ void build_static_tables(jacobi3d* c) {
     // the block width, else 128x30 (15 consumer warps) for wide blocks, 96x16
     // one-cell-per-lane tiles for 96-wide blocks (BASELINE configs[4]) and
     // 64x16 (2 CTAs/SM, 6 stages) for other narrow ones.  Sweeps: profiles/.
-    c->tile_kind = (c->nx % 192 == 0) ? 0 : c->nx >= 128 ? 1 : (c->nx == 96) ? 12 : 4;
+    // 96-wide blocks (BASELINE configs[4]): 96x16 one-cell-per-lane tiles, 4 warps x 4 rows,
+    // 7 stages (round 2: 333 -> 348 GLUPS persistent on 96^3 blocks, profiles/r02_tuning_log.md)
+    // (strategy C keeps 96x16 x 8 warps: kind 23's 7 stages leave no room for the y
+    // side rows its TMA-fed prologue needs, 283 vs 181 GLUPS batched)
+    c->tile_kind = (c->nx % 192 == 0) ? 0 : c->nx >= 128 ? 1 : (c->nx == 96) ? (c->cfg.variant == J3D_FUSE_C ? 12 : 23) : 4;
     if (c->tile_kind == 0) {
         // 192x24 (12 consumer warps) when 22-row tiles would leave a mostly empty last
         // tile row: measured on 192x96x96 blocks 1144 -> 1248 GLUPS (4 GPUs), equal at 1536
