@@ -332,14 +332,14 @@ def main():
         if a.launch == "per_block":
             # per-block launches run concurrently on their own streams: their
             # event times overlap, so use all stencil bytes over the step time
-            achieved = prof_bytes / (ms * a.steps * 1e-3) / 1e9
+            achieved = prof_bytes / (ms * a.steps * len(reps) * 1e-3) / 1e9
         tr, tr_src = traffic_from_profiles(a.workload, a.launch, a.variant, st.get("tile_kind"), a.steps)
         roof = {"bound": "hbm", "kernel": "stencil_tma_kernel", "achieved": round(achieved, 1), "peak": peak,
                 "unit": "GB/s", "frac": round(achieved / peak, 4),
                 "traffic": tr["traffic_bytes_per_launch"] if tr else None, "traffic_source": tr_src,
                 "tile_kind": st.get("tile_kind"),
                 "alg_bytes_per_launch": prof_bytes / prof_n, "avg_launch_ms": avg_ms,
-                "share_of_step": round(prof_ms / (ms * a.steps), 4), "peak_source": peak_src,
+                "share_of_step": round(prof_ms / (ms * a.steps * len(reps)), 4), "peak_source": peak_src,
                 "method": ("stencil bytes in the timed region / step time (per-block launches overlap)"
                            if a.launch == "per_block" else
                            "algorithmic bytes per launch / mean CUDA-event launch time")}
