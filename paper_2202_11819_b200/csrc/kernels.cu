@@ -408,6 +408,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
         int s = 0, qs = 0;
         uint32_t ph = 0, qph = 0;
         const int tma_mode = (flags >> 2) & 3;
+        const bool prefetch = !(flags & 16);  // claim the next item when this one starts (J3D_PREFETCH)
         const int total = n_items * ctl.n_iter;
         // lane 0 claims items and issues every TMA load; the whole warp polls the
         // persistent launch's dependency counters.  The next item is claimed when
@@ -419,7 +420,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
             if (g >= total) g = -1;
             int gn = 0;
             if (lane == 0) {
-                if (g >= 0) gn = (int)atomicAdd(&sched[0], 1u);
+                if (prefetch && g >= 0) gn = (int)atomicAdd(&sched[0], 1u);
                 mbar_wait(&qempty[qs], qph ^ 1);
                 queue[qs] = g;
                 mbar_arrive(&qfull[qs]);
@@ -487,6 +488,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                     }
                     if (++s == NSTAGE) { s = 0; ph ^= 1; }
                 }
+                if (!prefetch) gn = (int)atomicAdd(&sched[0], 1u);
             }
             g = __shfl_sync(0xffffffffu, gn, 0);
         }
@@ -1206,7 +1208,7 @@ static cudaError_t launch_t(const StencilLaunch& L, cudaStream_t st) {
     if (L.n_items <= 0) return cudaSuccess;
     stencil_tma_kernel<T><<<L.grid, T::THREADS, T::SMEM_BYTES, st>>>(
         L.descs, L.tmaps, L.tmaps_pro, L.tmaps_x, L.items, L.n_items, L.parity,
-        (L.faces ? 1 : 0) | ((L.tma_mode & 3) << 2), L.sched, L.ctl);
+        (L.faces ? 1 : 0) | ((L.tma_mode & 3) << 2) | (L.prefetch ? 0 : 16), L.sched, L.ctl);
     return cudaGetLastError();
 }
 

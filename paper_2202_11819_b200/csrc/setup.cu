@@ -375,8 +375,12 @@ void build_static_tables(jacobi3d* c) {
         // tile row: measured on 192x96x96 blocks 1144 -> 1248 GLUPS (4 GPUs), equal at 1536
         auto waste = [&](int ty) { return (double)(((c->ny + ty - 1) / ty) * ty - c->ny) / (double)c->ny; };
         if (waste(24) + 0.005 < waste(22)) c->tile_kind = 21;
+        // the largest blocks (1536^3, BASELINE configs[1]): 192x24 with 6 warps x 4 rows --
+        // fewer per-plane instructions per update, which matters under the 1 kW cap
+        // (374 -> 384 GLUPS, profiles/r02_tuning_log.md)
+        if (c->ny >= 1536 && c->ny % 24 == 0) c->tile_kind = 26;
     }
-    if (c->tile_kind <= 1 || c->tile_kind == 21) {  // small grids: the wide tiles cannot keep every SM busy -> 64x16, 2 CTAs/SM
+    if (c->tile_kind <= 1 || c->tile_kind == 21 || c->tile_kind == 26) {  // small grids: the wide tiles cannot keep every SM busy -> 64x16, 2 CTAs/SM
         const TileShape t = tile_shape(c->tile_kind);
         const int64_t tiles = ((c->nx + t.tx - 1) / t.tx) * ((c->ny + t.ty - 1) / t.ty) * nl;
         const int64_t max_items = tiles * std::max<int64_t>(1, c->nz / 24);
@@ -422,6 +426,7 @@ void build_static_tables(jacobi3d* c) {
         }
     CK(cudaMemcpy(c->d_tmaps_x, xmaps.data(), xmaps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
     if (const char* e = std::getenv("J3D_TMA_HINT")) c->tma_mode = std::atoi(e) % 3;
+    if (const char* e = std::getenv("J3D_PREFETCH")) c->prefetch = std::atoi(e) != 0;
 
     // ---- work items: per block, z-chunk outer, then ty, tx (x fastest), peer-face blocks first
     int occ = 1;

@@ -194,6 +194,49 @@ def run_graph_refused(G, grid):
     return "graph refused on a shared GPU"
 
 
+def run_fullsize(G):
+    """bench.py's 2-GPU weak-scaling grid at full size (1536^3 per rank, 1536 x 1536
+    x 3072, 116 GB on one B200): sampled cells on both sides of the inter-rank face
+    and random ones, bitwise against the oracle on each cell's dependency cone, for
+    the direct variant batched and persistent (P2P stores + epoch flags / cross-rank
+    slab counters)."""
+    from tests.helpers import cone_value
+
+    grid, seed, n = (1536, 1536, 3072), 20220223, 3
+    checked = []
+
+    for launch in ("batched", "persistent"):
+        def body(rank):
+            rng = np.random.default_rng(100 + rank)
+            ctx = G.create(rank, grid, odf=1, variant="direct", exchange="p2p", launch=launch)
+            try:
+                ctx.init("hash", seed=seed)
+                ctx.iterate(n)
+                ctx.synchronize()
+                out = []
+                for b in range(ctx.n_blocks):
+                    (ox, oy, oz), (ex, ey, ez), owner = ctx.block_info(b)
+                    if owner != rank:
+                        continue
+                    cells = [(int(rng.integers(ox, ox + ex)), int(rng.integers(oy, oy + ey)), z)
+                             for z in (oz, oz + ez - 1) for _ in range(4)]  # both sides of the rank face
+                    cells += [(int(rng.integers(ox, ox + ex)), int(rng.integers(oy, oy + ey)),
+                               int(rng.integers(oz, oz + ez))) for _ in range(4)]
+                    cells += [(0, 0, oz), (ex - 1, ey - 1, oz + ez - 1)]
+                    for (i, j, k) in cells:
+                        out.append(((i, j, k), ctx.get_region(b, (i - ox, j - oy, k - oz), (1, 1, 1))[0, 0, 0]))
+                return out
+            finally:
+                ctx.close()
+
+        for part in G.run(body):
+            for cell, got in part:
+                want = cone_value(grid, seed, n, cell)
+                assert np.float64(got).tobytes() == np.float64(want).tobytes(), (launch, cell, got, want)
+                checked.append(cell)
+    return f"full size 1536^3 x 2 ranks: {len(checked)} sampled cells bitwise"
+
+
 def cases_for(nr, which):
     """(grid, odf, variant, launch, graph, exchange, n, kind, seed[, overlap[, calls]])."""
     g = {2: (48, 40, 64), 4: (48, 64, 64), 8: (48, 48, 48)}[nr]
@@ -269,6 +312,9 @@ def main():
             if os.environ.get("J3D_GROUP_FAILFAST"):
                 raise SystemExit(f"first failure after {n} cases")
 
+    if which == "fullsize":
+        attempt(run_fullsize, ThreadGroup(2))
+        ranks = []
     for nr in ranks:
         G = ThreadGroup(nr)
         g = {2: (48, 40, 64), 4: (48, 64, 64), 8: (48, 48, 48)}[nr]

@@ -45,3 +45,10 @@ def test_eight_ranks_one_gpu():
     """BASELINE.json's 8-GPU GPU grid (2,2,2): every block face kind is a peer
     face; P2P, host staging, overlap and the persistent launch."""
     _run("quick", "8")
+
+
+def test_two_ranks_one_gpu_fullsize():
+    """bench.py's 2-GPU weak-scaling grid at full size (1536^3 per rank) with both
+    ranks on one GPU (116 GB): sampled cells bitwise against the oracle's
+    dependency cones, batched and persistent."""
+    _run("fullsize")
