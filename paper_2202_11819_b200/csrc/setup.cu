@@ -441,9 +441,9 @@ void build_static_tables(jacobi3d* c) {
     // chunk re-reads only 2 extra planes (2% at 96).  Measured sweep: 96
     // beats 32/64/128/full depth (profiles/).
     int64_t best_zc = std::max<int64_t>(1, (c->nz + 95) / 96);
-    // small problems: shorter chunks until there are >= 6 items per CTA slot
-    // (at least 24 planes per chunk): the last round of items is then short
-    // (measured: 96^3 blocks, ODF 64: 198 -> 225 GLUPS)
+    // small problems: shorter chunks until there are >= 8 items per CTA slot
+    // (at least 16 planes per chunk): the last round of items is then short
+    // (measured: 96^3 blocks, ODF 64: 198 -> 225 GLUPS in round 1 with >= 6 / 24)
     if (c->cfg.launch == J3D_PERSISTENT) {
         // persistent launch: iterations overlap, so there is no per-iteration tail to
         // shorten -- two items per CTA slot keep the SMs busy, and longer chunks re-read
@@ -451,7 +451,8 @@ void build_static_tables(jacobi3d* c) {
         // single block: 16 planes, 284 -> 342 GLUPS)
         while (tiles * best_zc < 2 * (int64_t)c->grid_cap && c->nz / (best_zc + 1) >= 16) ++best_zc;
     } else {
-        while (tiles * best_zc < 6 * (int64_t)c->grid_cap && c->nz / (best_zc + 1) >= 24) ++best_zc;
+        // (round 2: >= 8 items per CTA slot, >= 16 planes: 96^3 blocks batched 297 -> 306 GLUPS)
+        while (tiles * best_zc < 8 * (int64_t)c->grid_cap && c->nz / (best_zc + 1) >= 16) ++best_zc;
     }
     if (const char* e = std::getenv("J3D_ZCHUNK")) {  // tuning override: planes per z chunk
         const int64_t L = std::atoll(e);
