@@ -182,6 +182,17 @@ J3D_API int jacobi3d_plan(const jacobi3d_config *cfg, jacobi3d_plan_info *out);
 J3D_API int jacobi3d_debug_slab_deps(const jacobi3d_config *cfg, int32_t tile_ty, int32_t nzc, int64_t *host_out,
                                      int64_t cap_rows, int64_t *n_rows);
 
+/* Debug (no GPU): the shared-memory control plane of a multi-rank context on
+ * its own (control.cu; the one the P2P and host-staging backends use for
+ * barriers and reductions).  Rank `rank` of `n_ranks` (>= 2; every rank calls
+ * this concurrently -- threads or processes of one node -- with the same key
+ * and rounds) runs `rounds` collectives: out_sum[r] = sum over ranks of
+ * values[r] (mod 2^64), out_max[r] = max over ranks of values[r], with an
+ * extra barrier every third round.  J3D_ETIMEOUT if a rank does not show up
+ * within J3D_TIMEOUT_S. */
+J3D_API int jacobi3d_debug_control(const uint8_t *key, int32_t rank, int32_t n_ranks, int64_t rounds,
+                                   const uint64_t *values, uint64_t *out_sum, uint64_t *out_max);
+
 /* Fill out[128] with an NCCL unique id (call on rank 0 only, broadcast the
  * bytes to every rank before jacobi3d_create). */
 J3D_API int jacobi3d_nccl_unique_id(uint8_t out[128]);

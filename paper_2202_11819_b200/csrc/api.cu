@@ -142,6 +142,34 @@ int jacobi3d_debug_slab_deps(const jacobi3d_config* cfg, int32_t tile_ty, int32_
     });
 }
 
+int jacobi3d_debug_control(const uint8_t* key, int32_t rank, int32_t n_ranks, int64_t rounds, const uint64_t* values,
+                           uint64_t* out_sum, uint64_t* out_max) {
+    jacobi3d c;  // host-side state only: the control plane of a context, no device
+    return guarded([&]() -> int {
+        if (!key || !values || !out_sum || !out_max || rounds < 0) return fail(J3D_EINVAL, "NULL argument");
+        if (n_ranks < 2 || rank < 0 || rank >= n_ranks) return fail(J3D_EINVAL, "rank / n_ranks out of range");
+        c.rank = rank;
+        c.n_gpus = n_ranks;
+        uint64_t h = 1469598103934665603ULL;  // the job key exactly as jacobi3d_create derives it
+        for (int i = 0; i < 128; ++i) h = (h ^ key[i]) * 1099511628211ULL;
+        c.job_key = h;
+        struct Teardown {
+            jacobi3d* p;
+            ~Teardown() { ctl_teardown(p); }
+        } td{&c};
+        ctl_setup_own(&c);
+        ctl_connect(&c);
+        ctl_barrier(&c);
+        for (int64_t r = 0; r < rounds; ++r) {
+            out_sum[r] = ctl_reduce(&c, values[r], false);
+            out_max[r] = ctl_reduce(&c, values[r], true);
+            if (r % 3 == 2) ctl_barrier(&c);
+        }
+        ctl_barrier(&c);  // every rank has read every slot before the segments go
+        return J3D_OK;
+    });
+}
+
 int jacobi3d_nccl_unique_id(uint8_t out[128]) {
     return guarded([&]() -> int {
         if (!out) return fail(J3D_EINVAL, "out is NULL");

@@ -19,6 +19,8 @@
 
 #include <random>
 
+#include <sys/stat.h>
+
 using namespace j3d;
 
 namespace j3d {
@@ -42,13 +44,33 @@ CtlSeg* seg(jacobi3d* c, int r) { return reinterpret_cast<CtlSeg*>(c->ctl_base[r
 
 char* map_segment(const std::string& nm, bool create) {
     if (create) shm_unlink(nm.c_str());
-    const int fd = shm_open(nm.c_str(), create ? (O_CREAT | O_RDWR) : O_RDWR, 0600);
+    int fd = shm_open(nm.c_str(), create ? (O_CREAT | O_RDWR) : O_RDWR, 0600);
+    if (fd < 0 && !create) {  // a peer that has not created its segment yet: wait for it
+        const double limit = timeout_s();
+        const auto t0 = std::chrono::steady_clock::now();
+        while (fd < 0 && std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() < limit) {
+            std::this_thread::sleep_for(std::chrono::milliseconds(1));
+            fd = shm_open(nm.c_str(), O_RDWR, 0600);
+        }
+    }
     if (fd < 0)
-        throw Error(create ? J3D_ENOMEM : J3D_EINVAL,
+        throw Error(create ? J3D_ENOMEM : J3D_ETIMEOUT,
                     "shm_open " + nm + " failed" + (create ? "" : " (ranks must share one node)"));
     if (create && ftruncate(fd, (off_t)kCtlBytes) != 0) {
         close(fd);
         throw Error(J3D_ENOMEM, "ftruncate of the control segment failed");
+    }
+    if (!create) {  // the creator may not have sized it yet
+        const double limit = timeout_s();
+        const auto t0 = std::chrono::steady_clock::now();
+        struct stat sb;
+        while (fstat(fd, &sb) == 0 && sb.st_size < (off_t)kCtlBytes) {
+            if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit) {
+                close(fd);
+                throw Error(J3D_ETIMEOUT, "control segment " + nm + " was never sized");
+            }
+            std::this_thread::sleep_for(std::chrono::milliseconds(1));
+        }
     }
     void* p = mmap(nullptr, kCtlBytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
     close(fd);

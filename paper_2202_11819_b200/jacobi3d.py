@@ -84,6 +84,7 @@ def _load():
         "jacobi3d_profile_read": [P, ctypes.POINTER(D), ctypes.POINTER(I64), ctypes.POINTER(D)],
         "jacobi3d_set_skip_exchange": [P, ctypes.c_int],
         "jacobi3d_debug_slab_deps": [ctypes.POINTER(Config), I32, I32, P, I64, ctypes.POINTER(I64)],
+        "jacobi3d_debug_control": [P, I32, I32, I64, P, P, P],
         "jacobi3d_destroy": [P],
         "jacobi3d_div7_selftest": [U64, U64, ctypes.POINTER(U64), P],
     }
@@ -136,6 +137,19 @@ def debug_slab_deps(grid, odf=1, n_gpus=1, rank=0, tile_ty=1, nzc=1, block=(0, 0
     out = np.zeros((n.value, 7), dtype=np.int64)
     _ck(lib.jacobi3d_debug_slab_deps(ctypes.byref(cfg), tile_ty, nzc, out.ctypes.data, n.value, ctypes.byref(n)))
     return out
+
+
+def debug_control(key: bytes, rank: int, n_ranks: int, values) -> tuple[list[int], list[int]]:
+    """jacobi3d_debug_control (no GPU): sum and max over ranks of values[r] for every
+    round r through the shared-memory control plane; collective over n_ranks
+    concurrent callers (threads or processes) with the same key."""
+    vals = np.ascontiguousarray(np.asarray(values, dtype=np.uint64))
+    n = len(vals)
+    s_out = np.zeros(n, dtype=np.uint64)
+    m_out = np.zeros(n, dtype=np.uint64)
+    kb = (ctypes.c_uint8 * 128).from_buffer_copy(key)
+    _ck(lib.jacobi3d_debug_control(kb, rank, n_ranks, n, vals.ctypes.data, s_out.ctypes.data, m_out.ctypes.data))
+    return [int(x) for x in s_out], [int(x) for x in m_out]
 
 
 def nccl_unique_id() -> bytes:
