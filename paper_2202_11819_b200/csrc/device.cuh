@@ -47,16 +47,11 @@ struct StencilDesc {
     FaceRef pro[6];
 };
 
-// A unit of stencil work: one (TX x TY) tile of one block over planes [z0,z1),
-// marched upward (down == 0: z0 .. z1-1) or downward (down == 1: z1-1 .. z0).
-// Adjacent z chunks of a tile march in opposite directions, so the two planes
-// they share are loaded by both at the same moment (both chunks end -- or both
-// start -- there) and the second load hits L2 instead of DRAM.
+// A unit of stencil work: one (TX x TY) tile of one block over planes [z0,z1).
 struct WorkItem {
     int32_t blk;    // local block index (descriptor = 2*blk + parity)
     int16_t tx, ty; // tile coordinates
     int32_t z0, z1;
-    int32_t down;
 };
 
 // Multi-iteration (persistent) stencil launches, J3D_PERSISTENT: launch item g

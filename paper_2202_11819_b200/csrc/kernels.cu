@@ -403,13 +403,6 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    // Programmatic dependent launch (batched, one GPU: consecutive stencil launches,
-    // StencilLaunch::pdl): let the next launch's CTAs be scheduled onto SMs as ours
-    // retire and run the prologue above, then wait here until the previous grid has
-    // completed and its memory is visible -- before any read of its output or of the
-    // shared work counters.  Without the launch attribute both are no-ops.
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (warp == NCW) {  // ---------------- producer warp: item scheduling + TMA plane loads
         int s = 0, qs = 0;
@@ -467,10 +460,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                     for (int f = 0; f < 6; ++f)
                         if (ptma & (1u << f)) tmap_acquire(pm + f);
                 }
-                // planes in marching order: z0-1 .. z1 (up) or z1 .. z0-1 (down)
-                const int dz = w.down ? -1 : 1;
-                const int zbeg = w.down ? w.z1 : w.z0 - 1, zend = w.down ? w.z0 - 2 : w.z1 + 1;
-                for (int z = zbeg; z != zend; z += dz) {
+                for (int z = w.z0 - 1; z <= w.z1; ++z) {
                     mbar_wait(&empty[s], ph ^ 1);
                     mbar_expect_tx(&full[s], bytes);
                     unsigned char* dst = smem + s * T::STAGE_BYTES;
@@ -911,23 +901,20 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
             }
         };
 
-        // stages of planes z-1, z, z+1 are held; every value is read from smem.
-        // Marching direction dz: sb = the plane behind (z - dz), sa = the plane ahead.
-        const int dz = w.down ? -1 : 1;
-        const int zfirst = w.down ? w.z1 - 1 : w.z0;
-        acquire(zfirst - dz);
-        int sm = s;  // plane behind
+        // stages of planes z-1, z, z+1 are held; every value is read from smem
+        acquire(w.z0 - 1);
+        int sm = s;
         advance();
-        acquire(zfirst);
+        acquire(w.z0);
         int sc = s;
         advance();
-        for (int i = 0, z = zfirst; i < w.z1 - w.z0; ++i, z += dz) {
-            acquire(z + dz);
-            const int sp = s;  // plane ahead
+        for (int z = w.z0; z < w.z1; ++z) {
+            acquire(z + 1);
+            const int sp = s;
             advance();
-            const double* pm = stage(dz > 0 ? sm : sp) + sbase;  // plane z-1
+            const double* pm = stage(sm) + sbase;
             const double* pc = stage(sc) + sbase;
-            const double* pp = stage(dz > 0 ? sp : sm) + sbase;  // plane z+1
+            const double* pp = stage(sp) + sbase;
             const uint32_t fm = epi & (touch | (z == 0 ? 16u : 0u) | (z == nz - 1 ? 32u : 0u));
             using M0 = std::integral_constant<int, 0>;
             using M1 = std::integral_constant<int, 1>;
@@ -958,8 +945,8 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
         }
         __syncwarp();
         if (lane == 0) {
-            mbar_arrive(&empty[sm]);  // the last plane computed
-            mbar_arrive(&empty[sc]);  // the halo plane beyond it
+            mbar_arrive(&empty[sm]);  // plane z1-1
+            mbar_arrive(&empty[sc]);  // plane z1
         }
         if (ctl.done) {  // persistent launch: publish this warp's part of the item (release)
             const int sv = ctl.item_slab[it];
@@ -1219,24 +1206,10 @@ static cudaError_t launch_t(const StencilLaunch& L, cudaStream_t st) {
         attr_set.fetch_or(bit, std::memory_order_acq_rel);
     }
     if (L.n_items <= 0) return cudaSuccess;
-    const int flags = (L.faces ? 1 : 0) | ((L.tma_mode & 3) << 2) | (L.prefetch ? 0 : 16);
-    if (!L.pdl) {
-        stencil_tma_kernel<T><<<L.grid, T::THREADS, T::SMEM_BYTES, st>>>(
-            L.descs, L.tmaps, L.tmaps_pro, L.tmaps_x, L.items, L.n_items, L.parity, flags, L.sched, L.ctl);
-        return cudaGetLastError();
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)L.grid);
-    cfg.blockDim = dim3((unsigned)T::THREADS);
-    cfg.dynamicSmemBytes = T::SMEM_BYTES;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, stencil_tma_kernel<T>, L.descs, L.tmaps, L.tmaps_pro, L.tmaps_x, L.items,
-                              L.n_items, L.parity, flags, L.sched, L.ctl);
+    stencil_tma_kernel<T><<<L.grid, T::THREADS, T::SMEM_BYTES, st>>>(
+        L.descs, L.tmaps, L.tmaps_pro, L.tmaps_x, L.items, L.n_items, L.parity,
+        (L.faces ? 1 : 0) | ((L.tma_mode & 3) << 2) | (L.prefetch ? 0 : 16), L.sched, L.ctl);
+    return cudaGetLastError();
 }
 
 template <class T>

@@ -27,7 +27,6 @@ struct StencilLaunch {
     int kind;    // tile configuration (kernels.cu J3D_TILES)
     bool faces;  // any prologue/epilogue faces in this launch
     bool prefetch = false;   // the producer claims its next item when the current one starts
-    bool pdl = false;        // programmatic dependent launch after the previous kernel on the stream
     unsigned int* sched;     // device [2] scheduler counters (zero on entry; reset by the kernel)
     IterCtl ctl;             // iterations in this launch + slab dependency tracking (persistent)
 };

@@ -48,9 +48,6 @@ void stencil(jacobi3d* c, int begin, int count, int parity, cudaStream_t st, int
     L.kind = c->tile_kind;
     L.faces = c->faces_fused;
     L.prefetch = c->prefetch;
-    // programmatic dependent launch between consecutive batched stencil launches of a
-    // one-GPU context (no stream memory operation between them); not in graphs
-    L.pdl = c->pdl && c->n_gpus == 1 && c->cfg.launch == J3D_BATCHED && !c->capturing && c->persist_n == 0;
     L.sched = c->d_sched + 2 * (l + 1);  // one counter pair per concurrently running launch
     L.ctl = IterCtl{nullptr, nullptr, nullptr, 1, 0, 0, 0, 0};
     const int n_iter = c->persist_n;

@@ -427,7 +427,6 @@ void build_static_tables(jacobi3d* c) {
     CK(cudaMemcpy(c->d_tmaps_x, xmaps.data(), xmaps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
     if (const char* e = std::getenv("J3D_TMA_HINT")) c->tma_mode = std::atoi(e) % 3;
     if (const char* e = std::getenv("J3D_PREFETCH")) c->prefetch = std::atoi(e) != 0;
-    if (const char* e = std::getenv("J3D_PDL")) c->pdl = std::atoi(e) != 0;
 
     // ---- work items: per block, z-chunk outer, then ty, tx (x fastest), peer-face blocks first
     int occ = 1;
@@ -461,11 +460,6 @@ void build_static_tables(jacobi3d* c) {
     }
     int tile_order = 0;  // tuning override: tile order inside a z chunk
     if (const char* e = std::getenv("J3D_TILE_ORDER")) tile_order = std::atoi(e);
-    // z order (device.cuh WorkItem): 0 every chunk upward, z chunk outer; 1 odd chunks
-    // downward, z chunk outer; 2 odd chunks downward, z chunk fastest (every chunk of a
-    // tile in flight together)
-    int zorder = 1;
-    if (const char* e = std::getenv("J3D_ZORDER")) zorder = std::atoi(e);
     std::vector<WorkItem> items;
     c->item_begin.assign(nl, 0);
     c->item_count.assign(nl, 0);
@@ -476,30 +470,24 @@ void build_static_tables(jacobi3d* c) {
                (is_peer(l, 2) && w.ty == 0) || (is_peer(l, 3) && w.ty == nty - 1) ||
                (is_peer(l, 4) && w.z0 == 0) || (is_peer(l, 5) && w.z1 == c->nz);
     };
-    auto chunk_item = [&](int l, int64_t tx, int64_t ty, int64_t zc, std::vector<WorkItem>& out) {
-        const int z0 = (int)(c->nz * zc / best_zc), z1 = (int)(c->nz * (zc + 1) / best_zc);
-        if (z1 > z0) out.push_back(WorkItem{l, (int16_t)tx, (int16_t)ty, z0, z1, zorder >= 1 ? (int32_t)(zc & 1) : 0});
-    };
     for (int l : c->order) {
         c->item_begin[l] = (int)items.size();
-        if (zorder == 2) {  // z chunk fastest, tiles x fastest
-            for (int64_t ty = 0; ty < nty; ++ty)
+        for (int64_t zc = 0; zc < best_zc; ++zc) {
+            const int z0 = (int)(c->nz * zc / best_zc), z1 = (int)(c->nz * (zc + 1) / best_zc);
+            if (z1 <= z0) continue;
+            if (tile_order == 1) {  // y fastest
                 for (int64_t tx = 0; tx < ntx; ++tx)
-                    for (int64_t zc = 0; zc < best_zc; ++zc) chunk_item(l, tx, ty, zc, items);
-        } else {
-            for (int64_t zc = 0; zc < best_zc; ++zc) {
-                if (tile_order == 1) {  // y fastest
-                    for (int64_t tx = 0; tx < ntx; ++tx)
-                        for (int64_t ty = 0; ty < nty; ++ty) chunk_item(l, tx, ty, zc, items);
-                } else if (tile_order >= 2) {  // bands of `tile_order` tile rows, column-major inside a band
-                    for (int64_t b0 = 0; b0 < nty; b0 += tile_order)
-                        for (int64_t tx = 0; tx < ntx; ++tx)
-                            for (int64_t ty = b0; ty < std::min<int64_t>(nty, b0 + tile_order); ++ty)
-                                chunk_item(l, tx, ty, zc, items);
-                } else {  // x fastest
                     for (int64_t ty = 0; ty < nty; ++ty)
-                        for (int64_t tx = 0; tx < ntx; ++tx) chunk_item(l, tx, ty, zc, items);
-                }
+                        items.push_back(WorkItem{l, (int16_t)tx, (int16_t)ty, z0, z1});
+            } else if (tile_order >= 2) {  // bands of `tile_order` tile rows, column-major inside a band
+                for (int64_t b0 = 0; b0 < nty; b0 += tile_order)
+                    for (int64_t tx = 0; tx < ntx; ++tx)
+                        for (int64_t ty = b0; ty < std::min<int64_t>(nty, b0 + tile_order); ++ty)
+                            items.push_back(WorkItem{l, (int16_t)tx, (int16_t)ty, z0, z1});
+            } else {  // x fastest
+                for (int64_t ty = 0; ty < nty; ++ty)
+                    for (int64_t tx = 0; tx < ntx; ++tx)
+                        items.push_back(WorkItem{l, (int16_t)tx, (int16_t)ty, z0, z1});
             }
         }
         c->item_count[l] = (int)items.size() - c->item_begin[l];
