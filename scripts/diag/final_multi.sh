@@ -1,0 +1,18 @@
+timeout 1500 python -m pytest tests/test_gpu_multi.py -x -q > gpurun_out/r02_multi4_final.log 2>&1; echo multi rc=$?; tail -2 gpurun_out/r02_multi4_final.log
+run() { n=$1; shift; tag=$1; shift; python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port $((29500 + RANDOM % 400)) bench.py --gpus $n "$@" > gpurun_out/r02_final_n${n}_$tag.log 2>&1; echo "n=$n $tag rc=$?"; tail -1 gpurun_out/r02_final_n${n}_$tag.log | cut -c1-200; }
+run 2 weak1536_20 --steps 20 --warmup 5
+run 4 weak1536_20 --steps 20 --warmup 5
+run 2 weak1536_100 --steps 100 --warmup 10 --no-e2e
+run 4 weak1536_100 --steps 100 --warmup 10 --no-e2e
+run 2 fine384 --workload fine384_odf64 --steps 100 --warmup 10 --no-e2e
+run 4 fine384 --workload fine384_odf64 --steps 100 --warmup 10 --no-e2e
+run 2 fine768 --workload fine768_odf64 --steps 100 --warmup 10 --no-e2e
+run 4 fine768 --workload fine768_odf64 --steps 100 --warmup 10 --no-e2e
+run 4 small192 --workload small192_odf1 --steps 200 --warmup 10 --no-e2e
+run 4 strong1536 --workload strong1536_odf8 --steps 50 --warmup 5 --no-e2e
+run 4 weak1536_odf8 --workload weak1536_odf8 --steps 50 --warmup 5 --no-e2e
+run 4 weak1536_odf8_C --workload weak1536_odf8 --variant C --steps 50 --warmup 5 --no-e2e
+run 4 weak1536_host --steps 50 --warmup 5 --no-e2e --exchange host
+run 4 weak1536_host_ov --steps 50 --warmup 5 --no-e2e --exchange host --overlap 1
+run 4 weak1536_nccl --steps 50 --warmup 5 --no-e2e --exchange nccl
+run 4 fine384_batched --workload fine384_odf64 --launch batched --steps 100 --warmup 10 --no-e2e
