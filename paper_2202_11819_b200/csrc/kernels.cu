@@ -100,11 +100,14 @@ __device__ __forceinline__ void wait_counter(const unsigned int* p, uint32_t nee
 }
 
 // Called by the whole producer warp: lane j polls the item's j-th dependency
-// (one round trip for all of them instead of up to MAX_DEPS in sequence), then
-// lane 0 -- which issues the TMA loads -- orders them after every lane's
-// acquire (the warp barrier, a fence at the acquires' scope) and after the
-// generic-proxy writes they observed (proxy fence).
-__device__ __noinline__ void wait_slabs(const IterCtl ctl, int it, uint32_t iters, int lane) {
+// (one round trip for all of them instead of up to MAX_DEPS in sequence).
+// The warp barrier orders every lane's acquire before lane 0's later
+// operations (barriers are part of the causality order); lane 0 -- which
+// issues the TMA loads -- then orders the async proxy after the generic-proxy
+// writes those acquires observed.  (An extra fence at the acquires' scope,
+// `fence` = 1: J3D_DEPFENCE, measured for the record in
+// profiles/r02_tuning_log.md.)
+__device__ __noinline__ void wait_slabs(const IterCtl ctl, int it, uint32_t iters, int lane, bool fence) {
     const uint32_t need = iters * ctl.target;
     const unsigned int* const* dp = ctl.slab_deps + (int64_t)(ctl.item_slab[it] & SLAB_MASK) * MAX_DEPS;
     const uintptr_t p = lane < MAX_DEPS ? reinterpret_cast<uintptr_t>(dp[lane]) : 0;
@@ -112,8 +115,10 @@ __device__ __noinline__ void wait_slabs(const IterCtl ctl, int it, uint32_t iter
     if (p) wait_counter(reinterpret_cast<const unsigned int*>(p & ~uintptr_t(1)), need, (p & 1) != 0, ctl.timeout_ns);
     __syncwarp();
     if (lane == 0) {
-        if (ctl.sys) __threadfence_system();
-        else __threadfence();
+        if (fence) {
+            if (ctl.sys) __threadfence_system();
+            else __threadfence();
+        }
         asm volatile("fence.proxy.async.global;" ::: "memory");
     }
 }
@@ -430,7 +435,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
             const int k = g / n_items, it = g - k * n_items;
             // iteration 0 of a call waits only for peers (this GPU's previous
             // launch is complete in stream order)
-            if (ctl.done && (k > 0 || ctl.sys)) wait_slabs(ctl, it, ctl.base + (uint32_t)k, lane);
+            if (ctl.done && (k > 0 || ctl.sys)) wait_slabs(ctl, it, ctl.base + (uint32_t)k, lane, (flags & 32) != 0);
             if (lane == 0) {
                 uint64_t pol_first = 0, pol_last = 0;
                 if (tma_mode) {
@@ -1208,7 +1213,7 @@ static cudaError_t launch_t(const StencilLaunch& L, cudaStream_t st) {
     if (L.n_items <= 0) return cudaSuccess;
     stencil_tma_kernel<T><<<L.grid, T::THREADS, T::SMEM_BYTES, st>>>(
         L.descs, L.tmaps, L.tmaps_pro, L.tmaps_x, L.items, L.n_items, L.parity,
-        (L.faces ? 1 : 0) | ((L.tma_mode & 3) << 2) | (L.prefetch ? 0 : 16), L.sched, L.ctl);
+        (L.faces ? 1 : 0) | ((L.tma_mode & 3) << 2) | (L.prefetch ? 0 : 16) | (L.depfence ? 32 : 0), L.sched, L.ctl);
     return cudaGetLastError();
 }
 

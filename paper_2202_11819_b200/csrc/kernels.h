@@ -27,6 +27,7 @@ struct StencilLaunch {
     int kind;    // tile configuration (kernels.cu J3D_TILES)
     bool faces;  // any prologue/epilogue faces in this launch
     bool prefetch = false;   // the producer claims its next item when the current one starts
+    bool depfence = false;   // persistent: a gpu/sys fence after the dependency polling (experiment)
     unsigned int* sched;     // device [2] scheduler counters (zero on entry; reset by the kernel)
     IterCtl ctl;             // iterations in this launch + slab dependency tracking (persistent)
 };

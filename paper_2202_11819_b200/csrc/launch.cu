@@ -48,6 +48,7 @@ void stencil(jacobi3d* c, int begin, int count, int parity, cudaStream_t st, int
     L.kind = c->tile_kind;
     L.faces = c->faces_fused;
     L.prefetch = c->prefetch;
+    L.depfence = c->depfence;
     L.sched = c->d_sched + 2 * (l + 1);  // one counter pair per concurrently running launch
     L.ctl = IterCtl{nullptr, nullptr, nullptr, 1, 0, 0, 0, 0};
     const int n_iter = c->persist_n;

@@ -427,6 +427,7 @@ void build_static_tables(jacobi3d* c) {
     CK(cudaMemcpy(c->d_tmaps_x, xmaps.data(), xmaps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
     if (const char* e = std::getenv("J3D_TMA_HINT")) c->tma_mode = std::atoi(e) % 3;
     if (const char* e = std::getenv("J3D_PREFETCH")) c->prefetch = std::atoi(e) != 0;
+    if (const char* e = std::getenv("J3D_DEPFENCE")) c->depfence = std::atoi(e) != 0;
 
     // ---- work items: per block, z-chunk outer, then ty, tx (x fastest), peer-face blocks first
     int occ = 1;

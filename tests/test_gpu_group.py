@@ -18,12 +18,14 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _run(*args, timeout=1500):
+def _run(*args, timeout=900):
     env = dict(os.environ)
     # one hardware queue per stream: no rank's flag wait can sit in front of
     # work another rank's flag depends on (dist.ThreadGroup docstring)
     env["CUDA_DEVICE_MAX_CONNECTIONS"] = "32"
     env.setdefault("J3D_TIMEOUT_S", "120")
+    # a hang prints every thread's stack and exits instead of running into the timeout
+    env.setdefault("J3D_GROUP_DUMP_S", str(timeout - 60))
     p = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "group_worker.py"), *args],
                        capture_output=True, text=True, timeout=timeout, cwd=ROOT, env=env)
     assert p.returncode == 0 and "GROUP OK" in p.stdout, p.stdout[-4000:] + p.stderr[-4000:]
