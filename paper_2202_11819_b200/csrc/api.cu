@@ -234,7 +234,7 @@ int jacobi3d_create(const jacobi3d_config* cfg, const uint8_t* nccl_uid, jacobi3
         c->peer_base.assign(c->n_gpus, nullptr);
         build_static_tables(c);
         build_tables(c);
-        CK(preload_kernels(c->tile_kind));
+        CK(preload_kernels(c->tile_kind, c->tile_ys));
         CK(cudaStreamCreateWithFlags(&c->main, cudaStreamNonBlocking));
         int lo_pr = 0, hi_pr = 0;
         CK(cudaDeviceGetStreamPriorityRange(&lo_pr, &hi_pr));

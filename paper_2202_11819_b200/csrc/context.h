@@ -215,6 +215,7 @@ struct jacobi3d {
     std::vector<int> item_begin, item_count;  // per local block, in d_items
     std::vector<int64_t> item_cells;          // prefix sums of owned cells per item (profiling bytes)
     int n_items = 0, tile_kind = 0, grid_cap = 0;
+    bool tile_ys = false;                     // strategy C: the tile instance with y side rows (kernels.cu)
     bool depfence = false;                    // J3D_DEPFENCE=1: extra fence after the dependency polling (experiment)
     bool prefetch = false;                    // J3D_PREFETCH=1: claim the next work item when the current one starts
                                               // (measured slower: fine384 348 vs 353, 1536^3 376 vs 384 GLUPS)

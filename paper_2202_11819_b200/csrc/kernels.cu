@@ -236,7 +236,7 @@ __device__ __forceinline__ double sum7(double c, double xm, double xp, double ym
 // Tile shape: TX cells along x (a warp covers 64 with double2 per lane, CPL
 // column groups), NCW consumer warps each owning RPW rows (TY = NCW*RPW),
 // NSTAGE plane buffers in the TMA ring, MINB CTAs per SM targeted.
-template <int TX_, int NCW_, int RPW_, int NSTAGE_, int MINB_, int MAP_ = 0>
+template <int TX_, int NCW_, int RPW_, int NSTAGE_, int MINB_, int MAP_ = 0, bool YSREQ_ = false>
 struct Tile {
     static constexpr int TX = TX_, NCW = NCW_, RPW = RPW_, NSTAGE = NSTAGE_, MINB = MINB_;
     // MAP 0: a lane owns cell pairs (x, x+1), x = x0 + 64c + 2*lane (16-byte accesses);
@@ -262,8 +262,11 @@ struct Tile {
     static constexpr int YSIDE_STRIDE = (W * 8 + 127) / 128 * 128;
     static constexpr int BAR_BYTES = 2 * NSTAGE * 8 + 2 * 4 * 8 + 4 * 4 + 128;
     // the y side rows only where they keep MINB CTAs per SM (228 KB per SM, 1 KB
-    // reserved per CTA); otherwise strategy C patches y ghost rows generically
-    static constexpr bool YS = MINB * (NSTAGE * (YSIDE_OFF + 2 * YSIDE_STRIDE) + BAR_BYTES + 1024) <= 233472;
+    // reserved per CTA); otherwise strategy C patches y ghost rows generically.
+    // only in the instances strategy C launches (J3D_TILES_YS): the extra shared memory
+    // per stage costs the other variants up to 6 % (small192: 330 vs 350 GLUPS)
+    static constexpr bool YS =
+        YSREQ_ && MINB * (NSTAGE * (YSIDE_OFF + 2 * YSIDE_STRIDE) + BAR_BYTES + 1024) <= 233472;
     static constexpr int STAGE_BYTES = YS ? YSIDE_OFF + 2 * YSIDE_STRIDE : YSIDE_OFF;
     static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + BAR_BYTES;
     static constexpr int THREADS = 32 * (NCW + 1);
@@ -1226,6 +1229,17 @@ static cudaError_t occ_t(int* blocks) {
 }
 
 #define J3D_TYPE(k, tx, ncw, rpw, ns, mb) Tile<(tx > 0 ? tx : -tx), ncw, rpw, ns, mb, (tx > 0 ? 0 : 1)>
+#define J3D_TYPE_YS(k, tx, ncw, rpw, ns, mb) Tile<(tx > 0 ? tx : -tx), ncw, rpw, ns, mb, (tx > 0 ? 0 : 1), true>
+
+// The tile kinds strategy C uses by default (setup.cu) also get an instance with y
+// side rows for its TMA-fed prologue (same parameters as in J3D_TILES).
+#define J3D_TILES_YS(X)          \
+    X(0, 192, 11, 2, 5, 1)       \
+    X(1, 128, 15, 2, 5, 1)       \
+    X(4, 64, 8, 2, 6, 2)         \
+    X(12, -96, 8, 2, 6, 2)       \
+    X(21, 192, 12, 2, 5, 1)      \
+    X(26, 192, 6, 4, 5, 1)
 
 int num_tile_kinds() { return 28; }
 
@@ -1240,6 +1254,15 @@ TileShape tile_shape(int kind) {
 }
 
 cudaError_t launch_stencil(const StencilLaunch& L, cudaStream_t st) {
+    if (L.yside) {
+        switch (L.kind) {
+#define X(k, tx, ncw, rpw, ns, mb) \
+    case k: return launch_t<J3D_TYPE_YS(k, tx, ncw, rpw, ns, mb)>(L, st);
+            J3D_TILES_YS(X)
+#undef X
+        }
+        return cudaErrorInvalidValue;
+    }
     switch (L.kind) {
 #define X(k, tx, ncw, rpw, ns, mb) \
     case k: return launch_t<J3D_TYPE(k, tx, ncw, rpw, ns, mb)>(L, st);
@@ -1249,7 +1272,16 @@ cudaError_t launch_stencil(const StencilLaunch& L, cudaStream_t st) {
     return cudaErrorInvalidValue;
 }
 
-cudaError_t stencil_occupancy(int kind, bool, int* blocks_per_sm) {
+cudaError_t stencil_occupancy(int kind, bool ys, int* blocks_per_sm) {
+    if (ys) {
+        switch (kind) {
+#define X(k, tx, ncw, rpw, ns, mb) \
+    case k: return occ_t<J3D_TYPE_YS(k, tx, ncw, rpw, ns, mb)>(blocks_per_sm);
+            J3D_TILES_YS(X)
+#undef X
+        }
+        return cudaErrorInvalidValue;
+    }
     switch (kind) {
 #define X(k, tx, ncw, rpw, ns, mb) \
     case k: return occ_t<J3D_TYPE(k, tx, ncw, rpw, ns, mb)>(blocks_per_sm);
@@ -1273,13 +1305,22 @@ static cudaError_t preload_t() {
     return cudaFuncSetAttribute(stencil_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM_BYTES);
 }
 
-cudaError_t preload_kernels(int kind) {
+cudaError_t preload_kernels(int kind, bool ys) {
     cudaError_t e = cudaErrorInvalidValue;
-    switch (kind) {
+    if (ys) {
+        switch (kind) {
+#define X(k, tx, ncw, rpw, ns, mb) \
+    case k: e = preload_t<J3D_TYPE_YS(k, tx, ncw, rpw, ns, mb)>(); break;
+            J3D_TILES_YS(X)
+#undef X
+        }
+    } else {
+        switch (kind) {
 #define X(k, tx, ncw, rpw, ns, mb) \
     case k: e = preload_t<J3D_TYPE(k, tx, ncw, rpw, ns, mb)>(); break;
-        J3D_TILES(X)
+            J3D_TILES(X)
 #undef X
+        }
     }
     if (e != cudaSuccess) return e;
     cudaFuncAttributes a;
@@ -1294,8 +1335,8 @@ cudaError_t preload_kernels(int kind) {
 bool tile_yside(int kind) {
     switch (kind) {
 #define X(k, tx, ncw, rpw, ns, mb) \
-    case k: return J3D_TYPE(k, tx, ncw, rpw, ns, mb)::YS;
-        J3D_TILES(X)
+    case k: return J3D_TYPE_YS(k, tx, ncw, rpw, ns, mb)::YS;
+        J3D_TILES_YS(X)
 #undef X
     }
     return false;

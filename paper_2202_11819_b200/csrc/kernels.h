@@ -26,6 +26,7 @@ struct StencilLaunch {
     int grid;    // persistent CTAs
     int kind;    // tile configuration (kernels.cu J3D_TILES)
     bool faces;  // any prologue/epilogue faces in this launch
+    bool yside = false;      // launch the tile's instance with y side rows (strategy C)
     bool prefetch = false;   // the producer claims its next item when the current one starts
     bool depfence = false;   // persistent: a gpu/sys fence after the dependency polling (experiment)
     unsigned int* sched;     // device [2] scheduler counters (zero on entry; reset by the kernel)
@@ -35,11 +36,11 @@ struct StencilLaunch {
 int num_tile_kinds();
 TileShape tile_shape(int kind);
 int stencil_box_w(int kind);
-bool tile_yside(int kind);  // the tile's stages carry y side rows (strategy C's TMA-fed y ghost rows)
+bool tile_yside(int kind);  // the kind has an instance whose stages carry y side rows (strategy C's TMA-fed y ghost rows)
 int stencil_box_h(int kind);
 cudaError_t launch_stencil(const StencilLaunch& L, cudaStream_t st);
-cudaError_t stencil_occupancy(int kind, bool faces, int* blocks_per_sm);
-cudaError_t preload_kernels(int kind);  // defeat lazy loading (see kernels.cu)
+cudaError_t stencil_occupancy(int kind, bool ys, int* blocks_per_sm);
+cudaError_t preload_kernels(int kind, bool ys);  // defeat lazy loading (see kernels.cu)
 cudaError_t launch_div7_selftest(uint64_t n, uint64_t seed, unsigned long long* bad, double* example, int sms,
                                  cudaStream_t st);
 cudaError_t launch_wait_counters(const unsigned int* const* ptrs, int n, uint32_t need, uint64_t limit_ns,

@@ -47,6 +47,7 @@ void stencil(jacobi3d* c, int begin, int count, int parity, cudaStream_t st, int
     L.grid = std::min(count, c->grid_cap);
     L.kind = c->tile_kind;
     L.faces = c->faces_fused;
+    L.yside = c->tile_ys;
     L.prefetch = c->prefetch;
     L.depfence = c->depfence;
     L.sched = c->d_sched + 2 * (l + 1);  // one counter pair per concurrently running launch

@@ -172,7 +172,7 @@ void build_tables(jacobi3d* c) {
                         // its row stride is a multiple of 16 bytes (TMA); else the consumer
                         // warps patch them with generic loads (patch_stage)
                         const int64_t pitch_elems = c->face_na(f);
-                        const bool room = !(f == 2 || f == 3) || tile_yside(c->tile_kind);
+                        const bool room = !(f == 2 || f == 3) || c->tile_ys;
                         if (room && pitch_elems % 2 == 0 && ((uintptr_t)d.pro[f].p & 15) == 0) {
                             d.pro_tma |= 1u << f;
                             encode_recv_map(c, &pro_maps[(size_t)(2 * l + p) * 6 + f], d.pro[f].p, f);
@@ -391,6 +391,7 @@ void build_static_tables(jacobi3d* c) {
         if (k >= 0 && k < num_tile_kinds()) c->tile_kind = k;
     }
     const TileShape ts = tile_shape(c->tile_kind);
+    c->tile_ys = c->cfg.variant == J3D_FUSE_C && tile_yside(c->tile_kind);
     std::vector<CUtensorMap> maps(2 * nl);
     CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
     if (const char* e = std::getenv("J3D_L2PROMO")) {  // tuning override
@@ -431,7 +432,7 @@ void build_static_tables(jacobi3d* c) {
 
     // ---- work items: per block, z-chunk outer, then ty, tx (x fastest), peer-face blocks first
     int occ = 1;
-    CK(stencil_occupancy(c->tile_kind, false, &occ));
+    CK(stencil_occupancy(c->tile_kind, c->tile_ys, &occ));
     occ = std::max(1, occ);
     c->grid_cap = c->sms * occ;
     const int64_t ntx = (c->nx + ts.tx - 1) / ts.tx, nty = (c->ny + ts.ty - 1) / ts.ty;
