@@ -739,7 +739,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                     double* q = F.p + (int64_t)z * F.sb;
 #pragma unroll
                     for (int r = 0; r < RPW; ++r)
-                        if (yl + r < ny) {
+                        if (WHOLE || yl + r < ny) {
                             q[(int64_t)(yl + r) * F.sa] = cap0[r];
                         }
                 }
@@ -748,7 +748,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                     double* q = F.p + (int64_t)z * F.sb;
 #pragma unroll
                     for (int r = 0; r < RPW; ++r)
-                        if (yl + r < ny) {
+                        if (WHOLE || yl + r < ny) {
                             q[(int64_t)(yl + r) * F.sa] = cap1[r];
                         }
                 }
@@ -942,7 +942,8 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
                 }
             } else {
                 if (fm & ~3u) compute_plane(M2{}, std::false_type{}, z, fm, pm, pc, pp);
-                else if (fm) compute_plane(M1{}, std::false_type{}, z, fm, pm, pc, pp);
+                else if (fm && whole) compute_plane(M1{}, std::true_type{}, z, fm, pm, pc, pp);  // x faces only:
+                else if (fm) compute_plane(M1{}, std::false_type{}, z, fm, pm, pc, pp);          // half the tiles at ODF >= 8
                 else if (whole) compute_plane(M0{}, std::true_type{}, z, 0u, pm, pc, pp);
                 else compute_plane(M0{}, std::false_type{}, z, 0u, pm, pc, pp);
             }
