@@ -123,25 +123,33 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def lib_sha256():
-    """sha256 of the loaded libjacobi3d.so: ties an ncu capture to the build."""
+def build_sha256():
+    """sha256 over the library's sources and build script (csrc/, include/, build.py):
+    ties an ncu capture to the code it measured.  (Not the .so itself: nvcc output
+    is not bit-reproducible, so every rebuild of the same sources hashes differently.)"""
+    import glob
     import hashlib
 
-    from paper_2202_11819_b200 import jacobi3d as jb
-
-    with open(jb.LIB_PATH, "rb") as f:
-        return hashlib.sha256(f.read()).hexdigest()
+    h = hashlib.sha256()
+    pk = os.path.join(ROOT, "paper_2202_11819_b200")
+    files = sorted(glob.glob(os.path.join(pk, "csrc", "*")) + glob.glob(os.path.join(ROOT, "include", "*.h")) +
+                   [os.path.join(pk, "build.py")])
+    for f in files:
+        h.update(os.path.relpath(f, ROOT).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
 
 
 def traffic_from_profiles(workload, launch, variant, tile_kind, steps):
     """dram__bytes_read.sum + dram__bytes_write.sum per stencil launch from a
     committed ncu --set full summary (profiles/ncu_stencil_*.json) -- only one
-    captured from THIS build (sha256 of the library) with the same workload,
+    captured from THIS build (sha256 of the library's sources) with the same workload,
     launch mode, variant and tile kind (and, for the persistent launch, the
     same iterations per launch); otherwise None and the reason."""
     import glob
 
-    sha = lib_sha256()
+    sha = build_sha256()
     why = "no committed ncu capture for this workload"
     for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_stencil_*.json"))):
         try:
@@ -151,7 +159,7 @@ def traffic_from_profiles(workload, launch, variant, tile_kind, steps):
             continue
         if d.get("workload") != workload or not d.get("traffic_bytes_per_launch"):
             continue
-        want = {"lib_sha256": sha, "launch": launch, "variant": variant, "tile_kind": tile_kind}
+        want = {"build_sha256": sha, "launch": launch, "variant": variant, "tile_kind": tile_kind}
         if launch == "persistent":
             want["iters_per_launch"] = steps
         bad = [k for k, v in want.items() if d.get(k) != v]

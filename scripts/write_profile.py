@@ -55,12 +55,12 @@ def main():
     wr = to_bytes(*s["dram__bytes_write.sum"])
     dur_ms = float(s["gpu__time_duration.sum"][0])
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    import hashlib
+    sys.path.insert(0, ROOT)
+    import bench
 
-    with open(os.path.join(ROOT, "paper_2202_11819_b200", "libjacobi3d.so"), "rb") as f:
-        sha = hashlib.sha256(f.read()).hexdigest()  # the build the capture was taken with (bench.py checks it)
+    sha = bench.build_sha256()  # the sources the capture was taken with (bench.py checks it)
     js = {"round": a.round, "workload": a.workload, "launch": a.launch, "variant": a.variant,
-          "tile_kind": a.tile_kind, "iters_per_launch": a.iters_per_launch, "lib_sha256": sha,
+          "tile_kind": a.tile_kind, "iters_per_launch": a.iters_per_launch, "build_sha256": sha,
           "kernel": s.get("kernel"), "traffic_bytes_per_launch": rd + wr, "dram_read_bytes": rd,
           "dram_write_bytes": wr, "alg_bytes_per_launch": a.alg_bytes, "traffic_over_alg": (rd + wr) / a.alg_bytes,
           "ncu_duration_ms": dur_ms, "source": os.path.basename(a.rep),
