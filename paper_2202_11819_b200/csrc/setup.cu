@@ -499,6 +499,34 @@ void build_static_tables(jacobi3d* c) {
         }
         c->item_count[l] = (int)items.size() - c->item_begin[l];
     }
+    // Batched launch: the last round of the dynamic scheduler (the final grid_cap
+    // items) in half-height items, so the launch's tail -- SMs idle while the last
+    // items finish -- is half as long (J3D_TAILSPLIT=0: off)
+    int tail_split = 1;
+    if (const char* e = std::getenv("J3D_TAILSPLIT")) tail_split = std::atoi(e);
+    if (tail_split && c->cfg.launch == J3D_BATCHED && !c->overlap) {
+        // mode 1: the last grid_cap items in halves; mode 2: also the last grid_cap in
+        // quarters and the grid_cap before them in halves
+        const size_t n0 = items.size(), k = std::min(n0, (size_t)c->grid_cap);
+        std::vector<WorkItem> out;
+        out.reserve(n0 + 4 * k);
+        for (size_t i = 0; i < n0; ++i) {
+            const WorkItem& w = items[i];
+            int parts = 1;
+            if (i >= n0 - k) parts = tail_split >= 2 ? 4 : 2;
+            else if (tail_split >= 2 && i + 2 * k >= n0) parts = 2;
+            while (parts > 1 && (w.z1 - w.z0) / parts < 4) parts /= 2;
+            for (int q = 0; q < parts; ++q)
+                out.push_back(WorkItem{w.blk, w.tx, w.ty, w.z0 + (w.z1 - w.z0) * q / parts,
+                                       w.z0 + (w.z1 - w.z0) * (q + 1) / parts});
+        }
+        items.swap(out);
+        for (int l = 0; l < nl; ++l) c->item_count[l] = 0;
+        for (size_t i = 0; i < items.size(); ++i) {  // blocks stay contiguous in the list
+            const int l = items[i].blk;
+            if (c->item_count[l]++ == 0) c->item_begin[l] = (int)i;
+        }
+    }
     c->n_ext = 0;
     if (c->overlap) {  // BATCHED only: exterior items of every block first (stable order otherwise)
         std::stable_partition(items.begin(), items.end(), exterior);
