@@ -70,3 +70,38 @@ def test_weak_scaling_grids_plan_to_fixed_per_gpu_work():
             if wl["odf"] == 1:
                 assert info["peer_faces_max"] == faces, (name, n, info)
             assert 0 < info["bytes_per_gpu"] < 180e9, (name, n, info["bytes_per_gpu"])
+
+
+def test_traffic_only_from_a_matching_capture(tmp_path, monkeypatch):
+    """roofline.traffic comes from a committed ncu capture only when it was taken from
+    the same sources (build_sha256), workload, launch mode, variant, tile kind and --
+    for the persistent launch -- iterations per launch; otherwise None and the reason."""
+    import shutil
+
+    sys.path.insert(0, ROOT)
+    import bench
+
+    sha = bench.build_sha256()
+    assert sha == bench.build_sha256() and len(sha) == 64  # deterministic over the sources
+    prof = tmp_path / "profiles"
+    prof.mkdir()
+    cap = {"workload": "weak1536_odf1", "launch": "batched", "variant": "direct", "tile_kind": 26,
+           "iters_per_launch": 1, "build_sha256": sha, "traffic_bytes_per_launch": 5.9e10}
+    (prof / "ncu_stencil_x.json").write_text(json.dumps(cap))
+    # build_sha256 hashes ROOT's sources: give the temporary root the same ones
+    for sub in ("paper_2202_11819_b200/csrc", "include"):
+        shutil.copytree(os.path.join(ROOT, sub), tmp_path / sub)
+    shutil.copy(os.path.join(ROOT, "paper_2202_11819_b200", "build.py"), tmp_path / "paper_2202_11819_b200")
+    monkeypatch.setattr(bench, "ROOT", str(tmp_path))
+    d, src = bench.traffic_from_profiles("weak1536_odf1", "batched", "direct", 26, 20)
+    assert d and d["traffic_bytes_per_launch"] == 5.9e10 and src == "ncu_stencil_x.json"
+    assert bench.traffic_from_profiles("weak1536_odf1", "batched", "direct", 0, 20)[0] is None  # tile kind
+    assert bench.traffic_from_profiles("weak1536_odf1", "persistent", "direct", 26, 20)[0] is None  # launch
+    cap.update(launch="persistent", iters_per_launch=100)
+    (prof / "ncu_stencil_x.json").write_text(json.dumps(cap))
+    assert bench.traffic_from_profiles("weak1536_odf1", "persistent", "direct", 26, 100)[0] is not None
+    assert bench.traffic_from_profiles("weak1536_odf1", "persistent", "direct", 26, 20)[0] is None  # iterations
+    with open(tmp_path / "paper_2202_11819_b200" / "csrc" / "kernels.cu", "a") as f:
+        f.write("// edited\n")
+    d, why = bench.traffic_from_profiles("weak1536_odf1", "persistent", "direct", 26, 100)
+    assert d is None and "build_sha256" in why  # a source edit invalidates the capture
