@@ -451,11 +451,13 @@ void build_static_tables(jacobi3d* c) {
         // shorten -- two items per CTA slot keep the SMs busy, and longer chunks re-read
         // fewer boundary planes (96^3 blocks: 24 -> 48 planes, 311 -> 330 GLUPS; 192^3
         // single block: 16 planes, 284 -> 342 GLUPS)
-        // Across GPUs, more items per slot: slabs next to a peer run last in each
+        // Across GPUs, chunks down to 12 planes: slabs next to a peer run last in each
         // iteration, and shorter chunks let the rest of the GPU run ahead while they
-        // wait (4 GPUs: 192x96x96 blocks 1276 -> 1315, one 192^3 block 832 -> 929,
-        // 96^3 blocks 1334 -> 1346 GLUPS; profiles/r02_tuning_log.md)
-        const int64_t per_slot = c->n_gpus > 1 ? 4 : 2, min_planes = c->n_gpus > 1 ? 12 : 16;
+        // wait (4 GPUs: one 192^3 block 832 -> 929 GLUPS).  Four items per slot
+        // helped too before the wavefront slab order below; with it, two (4 GPUs:
+        // 192x96x96 blocks, 48- instead of 32-plane chunks, 1337 -> 1375-1401 GLUPS;
+        // profiles/r02_tuning_log.md)
+        const int64_t per_slot = 2, min_planes = c->n_gpus > 1 ? 12 : 16;
         while (tiles * best_zc < per_slot * (int64_t)c->grid_cap && c->nz / (best_zc + 1) >= min_planes) ++best_zc;
     } else {
         // (round 2: >= 8 items per CTA slot, >= 16 planes: 96^3 blocks batched 297 -> 306 GLUPS)
