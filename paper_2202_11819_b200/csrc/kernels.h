@@ -19,7 +19,7 @@ struct StencilLaunch {
     const CUtensorMap* tmaps;  // device, [2*n_local_blocks], 64-B aligned
     const CUtensorMap* tmaps_pro;    // device, [2*n_local_blocks][6]: strategy C's receive buffers per face
     const CUtensorMap* tmaps_x;      // device, [2*n_local_blocks]: x ghost vectors (y, z, side), box TY x 1 x 1
-    int tma_mode;            // 0 plain, 1 evict_first, 2 evict_last (L2 policy experiments)
+    int tma_mode;            // L2 policy of the plane loads: 0 plain, 1 evict_first, 2 evict_last (default)
     const WorkItem* items;     // device
     int n_items;
     int parity;  // input buffer parity
