@@ -191,9 +191,9 @@ struct jacobi3d {
     CUtensorMap* d_tmaps = nullptr;
     CUtensorMap* d_tmaps_pro = nullptr;  // [2*l + p][6] strategy C: maps over the receive buffers the prologue reads
     CUtensorMap* d_tmaps_x = nullptr;  // [2*l + p] x ghost vectors of each buffer
-    // L2 policy of the stencil's plane loads: evict_last (2) keeps the input planes --
-    // whose halo rows / columns neighbouring tiles read again -- ahead of the output
-    // lines in L2 (1536^3: 383.0 -> 388.5 GLUPS over 100 steps, profiles/r02_tuning_log.md);
+    // L2 policy of the stencil's plane loads: evict_last (2) ranks the input planes ahead
+    // of the output lines in L2.  Measured: 1536^3 383.0 -> 388.5 GLUPS over 100 steps with
+    // the same DRAM bytes (ncu 1.033x) in a shorter launch (profiles/r02_tuning_log.md);
     // J3D_TMA_HINT=0 / 1: plain / evict_first
     int tma_mode = 2;
     WorkItem* d_items = nullptr;
