@@ -53,7 +53,8 @@ def main():
     s = summary(a.rep)[0]
     rd = to_bytes(*s["dram__bytes_read.sum"])
     wr = to_bytes(*s["dram__bytes_write.sum"])
-    dur_ms = float(s["gpu__time_duration.sum"][0])
+    dv, du = s["gpu__time_duration.sum"]
+    dur_ms = float(dv) * {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "s": 1e3}.get(du, 1.0)
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     sys.path.insert(0, ROOT)
     import bench
